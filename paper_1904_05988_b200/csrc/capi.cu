@@ -1,0 +1,179 @@
+// extern "C" entry points: transforms (transform.hpp:54-96) and the ImexOde operators
+// (swe.hpp:44-79). All data pointers are device pointers; see include/pswe.h.
+#include "pswe_internal.h"
+
+using namespace pswe;
+
+namespace {
+
+void need(const void* p, const char* what) {
+    if (!p) throw std::invalid_argument(std::string(what) + " is NULL");
+}
+
+inline const double2* c2(const double* p) { return reinterpret_cast<const double2*>(p); }
+inline double2* c2(double* p) { return reinterpret_cast<double2*>(p); }
+
+int batch_groups(int n, int per) { return (n + per - 1) / per; }
+
+}  // namespace
+
+namespace pswe {
+
+// eval_implicit + eval_explicit of n states: the hot path (swe.cpp:9-69).
+// 4 launches: inverse Legendre (Phi, zeta, U, V) -> fused FFT/products/FFT -> forward Legendre
+// (5 projections) -> tail (tendency assembly + linear operator).
+void eval_imex(pswe_plan& P, const pswe_params& prm, const double2* state, double2* f_imp, double2* f_exp,
+               int n, cudaStream_t st) {
+    P.reserve(n);
+    legendre_inverse(P, INV_EVAL, state, nullptr, n, prm.radius, P.d_four_a, st);
+    fft_eval_products(P, prm, P.d_four_a, P.d_four_b, n, st);
+    legendre_forward(P, P.d_four_b, 5, n, P.d_proj, true, st);
+    eval_tail(P, prm, P.d_proj, state, f_imp, f_exp, n, st);
+}
+
+}  // namespace pswe
+
+extern "C" {
+
+int pswe_synthesise(pswe_plan* P, const double* coeffs, double* grid, int n, void* stream) {
+    return guarded([&] {
+        need(P, "plan");
+        need(coeffs, "coeffs");
+        need(grid, "grid");
+        if (n <= 0) return;
+        P->reserve(batch_groups(n, 5));
+        legendre_inverse(*P, INV_PLAIN, c2(coeffs), nullptr, n, 1.0, P->d_four_a, as_stream(stream));
+        fft_rows_c2r(*P, P->d_four_a, 1, 0, grid, n, false, as_stream(stream));
+    });
+}
+
+int pswe_analyse(pswe_plan* P, const double* grid, double* coeffs, int n, void* stream) {
+    return guarded([&] {
+        need(P, "plan");
+        need(coeffs, "coeffs");
+        need(grid, "grid");
+        if (n <= 0) return;
+        P->reserve(batch_groups(n, 5));
+        fft_rows_r2c(*P, grid, P->d_four_a, 1, 0, n, false, 0, 1.0, as_stream(stream));
+        legendre_forward(*P, P->d_four_a, n, 1, c2(coeffs), false, as_stream(stream));
+    });
+}
+
+int pswe_uv_from_vortdiv(pswe_plan* P, const double* vort, const double* div, double radius, double* u,
+                         double* v, int n, void* stream) {
+    return guarded([&] {
+        need(P, "plan");
+        need(vort, "vort");
+        need(div, "div");
+        need(u, "u");
+        need(v, "v");
+        if (n <= 0) return;
+        P->reserve(batch_groups(2 * n, 5));
+        const cudaStream_t st = as_stream(stream);
+        legendre_inverse(*P, INV_UV, c2(vort), c2(div), n, radius, P->d_four_a, st);
+        fft_rows_c2r(*P, P->d_four_a, 2, 0, u, n, true, st);
+        fft_rows_c2r(*P, P->d_four_a, 2, 1, v, n, true, st);
+    });
+}
+
+int pswe_vortdiv_from_uv(pswe_plan* P, const double* u, const double* v, double radius, double* vort,
+                         double* div, int n, void* stream) {
+    return guarded([&] {
+        need(P, "plan");
+        need(vort, "vort");
+        need(div, "div");
+        need(u, "u");
+        need(v, "v");
+        if (n <= 0) return;
+        P->reserve(batch_groups(2 * n, 5));
+        const cudaStream_t st = as_stream(stream);
+        fft_rows_r2c(*P, u, P->d_four_a, 2, 0, n, true, 1, radius, st);
+        fft_rows_r2c(*P, v, P->d_four_a, 2, 1, n, true, 1, radius, st);
+        legendre_forward(*P, P->d_four_a, 2, n, P->d_proj, true, st);
+        vortdiv_tail(*P, P->d_proj, c2(vort), c2(div), n, st);
+    });
+}
+
+int pswe_laplacian(int R, const double* x, double radius, double* y, int n, int inverse, void* stream) {
+    return guarded([&] {
+        need(x, "x");
+        need(y, "y");
+        if (R < 1) throw std::invalid_argument("laplacian: truncation must be >= 1");
+        laplacian(R, c2(x), radius, c2(y), n, inverse != 0, as_stream(stream));
+    });
+}
+
+int pswe_eval_explicit(pswe_plan* P, const pswe_params* p, const double* state, double* f_exp, int n,
+                       void* stream) {
+    return guarded([&] {
+        need(P, "plan");
+        need(p, "params");
+        need(state, "state");
+        need(f_exp, "f_exp");
+        if (n <= 0) return;
+        eval_imex(*P, *p, c2(state), nullptr, c2(f_exp), n, as_stream(stream));
+    });
+}
+
+int pswe_eval_implicit(int R, const pswe_params* p, const double* state, double* f_imp, int n, void* stream) {
+    return guarded([&] {
+        need(p, "params");
+        need(state, "state");
+        need(f_imp, "f_imp");
+        if (R < 1) throw std::invalid_argument("eval_implicit: truncation must be >= 1");
+        eval_linear(R, *p, c2(state), c2(f_imp), n, as_stream(stream));
+    });
+}
+
+int pswe_eval_imex(pswe_plan* P, const pswe_params* p, const double* state, double* f_imp, double* f_exp, int n,
+                   void* stream) {
+    return guarded([&] {
+        need(P, "plan");
+        need(p, "params");
+        need(state, "state");
+        need(f_imp, "f_imp");
+        need(f_exp, "f_exp");
+        if (n <= 0) return;
+        eval_imex(*P, *p, c2(state), c2(f_imp), c2(f_exp), n, as_stream(stream));
+    });
+}
+
+// eval_imex with CUDA events between its 4 launches on `stream`; synchronises and writes the
+// per-stage device times (ms) to ms_out[4]: inverse Legendre, fused FFT/products, forward
+// Legendre, tail. Used by bench.py for the per-kernel roofline.
+int pswe_eval_imex_timed(pswe_plan* P, const pswe_params* p, const double* state, double* f_imp, double* f_exp,
+                         int n, void* stream, float* ms_out) {
+    return guarded([&] {
+        need(P, "plan");
+        need(p, "params");
+        need(ms_out, "ms_out");
+        const cudaStream_t st = as_stream(stream);
+        P->reserve(n);
+        cudaEvent_t ev[5];
+        for (auto& e : ev) PSWE_CUDA(cudaEventCreate(&e));
+        PSWE_CUDA(cudaEventRecord(ev[0], st));
+        legendre_inverse(*P, INV_EVAL, c2(state), nullptr, n, p->radius, P->d_four_a, st);
+        PSWE_CUDA(cudaEventRecord(ev[1], st));
+        fft_eval_products(*P, *p, P->d_four_a, P->d_four_b, n, st);
+        PSWE_CUDA(cudaEventRecord(ev[2], st));
+        legendre_forward(*P, P->d_four_b, 5, n, P->d_proj, true, st);
+        PSWE_CUDA(cudaEventRecord(ev[3], st));
+        eval_tail(*P, *p, P->d_proj, c2(state), c2(f_imp), c2(f_exp), n, st);
+        PSWE_CUDA(cudaEventRecord(ev[4], st));
+        PSWE_CUDA(cudaEventSynchronize(ev[4]));
+        for (int i = 0; i < 4; ++i) PSWE_CUDA(cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]));
+        for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
+int pswe_solve_implicit(int R, const pswe_params* p, const double* b, double c, double* out, int n, void* stream) {
+    return guarded([&] {
+        need(p, "params");
+        need(b, "b");
+        need(out, "out");
+        if (R < 1) throw std::invalid_argument("solve_implicit: truncation must be >= 1");
+        solve_implicit(R, *p, c2(b), c, c2(out), n, as_stream(stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,184 @@
+// Internal declarations of libpswe (B200 / sm_100a, fp64). See include/pswe.h for the ABI and
+// DESIGN.md for the data layout and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "pswe.h"
+
+namespace pswe {
+
+// ------------------------------------------------------------------------------------------
+// errors
+
+void set_error(const std::string& msg);
+
+#define PSWE_CUDA(x)                                                                          \
+    do {                                                                                      \
+        cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess)                                                                \
+            throw std::runtime_error(std::string(#x) + " failed: " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define PSWE_LAUNCH_CHECK() PSWE_CUDA(cudaGetLastError())
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return 1;
+    }
+}
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------------------------------
+// spectral indexing (field.hpp:29-32) and the "extended" triangle s = m..R+1 used internally
+
+__host__ __device__ inline long off_std(int R, int m) { return (long)m * (2 * R + 3 - m) / 2; }
+__host__ __device__ inline long off_ext(int R, int m) { return (long)m * (2 * R + 5 - m) / 2; }
+inline long num_coeffs(int R) { return (long)(R + 1) * (R + 2) / 2; }
+inline long num_ext(int R) { return (long)(R + 1) * (R + 4) / 2; }
+
+// ------------------------------------------------------------------------------------------
+// FFT descriptor: complex Stockham DIF of length N = nlon/2, radices 4/2/3/5
+
+struct FftStage {
+    int p;       // radix
+    int m;       // sub-length after this stage (n/p)
+    int s;       // stride
+    int tw_off;  // offset of this stage's twiddles tw[j*p + t] in Plan::d_fft_tw
+};
+constexpr int kMaxFftStages = 16;
+struct FftDesc {
+    int N;
+    int nst;
+    FftStage st[kMaxFftStages];
+};
+
+// ------------------------------------------------------------------------------------------
+// kernel launchers (defined in legendre.cu / fft.cu / ops.cu)
+
+struct DevPlan;  // POD view of the plan passed to kernels
+
+}  // namespace pswe
+
+// The plan: TransformPlan (transform.hpp:27-96) on one device. Immutable after creation except
+// for the grow-only scratch, which makes it single-stream (one host thread) like the ABI says.
+struct pswe_plan {
+    int R = 0, nlat = 0, nlon = 0, J = 0, N = 0;
+    int legendre_mode = PSWE_LEGENDRE_RECOMPUTE;
+    int device = 0;
+    long K = 0, Kx = 0;
+    // host copies
+    std::vector<double> mu, w, cosphi;
+    // device constants
+    double* d_mu_n = nullptr;    // [J] mu at north-half latitude j (row nlat/2 + j)
+    double* d_seed = nullptr;    // [(R+1) * J] P^m_m(mu_j) (legendre.cpp:26-29)
+    double2* d_rec = nullptr;    // [Kx] (1/eps(m,s+1), eps(m,s)/eps(m,s+1)) at off_ext(m)+s-m
+    double* d_eps = nullptr;     // [Kx] eps(m, s) at off_ext(m)+s-m, s = m..R+1
+    double* d_ptab = nullptr;    // STREAM mode: [Kx * J] P^m_s(mu_j), block m: [j][s]
+    double* d_rowc = nullptr;    // [nlat] cos(phi_i)
+    double* d_roww = nullptr;    // [nlat] Gauss weight w_i
+    double* d_rowmu = nullptr;   // [nlat] mu_i
+    double2* d_fft_tw = nullptr; // stage twiddles
+    double2* d_fft_post = nullptr;  // [N+1] exp(-2 pi i k / nlon)
+    pswe::FftDesc fft{};
+    // scratch (grow-only)
+    int cap_batch = 0;
+    double2* d_four_a = nullptr;  // [cap * 5 * (R+1) * nlat] Fourier rows, [b][f][m][i]
+    double2* d_four_b = nullptr;  // [cap * 5 * (R+1) * nlat]
+    double2* d_proj = nullptr;    // [cap * 5 * Kx] Legendre projections, extended layout
+    void reserve(int batch);
+};
+
+namespace pswe {
+
+// legendre.cu
+enum InvKind { INV_PLAIN = 0, INV_UV = 1, INV_EVAL = 2 };
+// Inverse Legendre (synthesis) into Fourier rows out[b][f][m][i].
+// PLAIN: in = n fields [K] (in2 unused); UV: in = n vort fields, in2 = n div fields;
+// EVAL: in = n states [3][K]. out rows: PLAIN [f][m][i], UV [b][2][m][i], EVAL [b][4][m][i].
+void legendre_inverse(const pswe_plan& P, int kind, const double2* in, const double2* in2, int n,
+                      double radius, double2* out, cudaStream_t st);
+// Forward Legendre (analysis) from Fourier rows four[b][f][m][i] (nf fields per batch item) into
+// projections; out_ext: extended layout [b][f][Kx] (s = m..R+1); else standard [b][f][K].
+void legendre_forward(const pswe_plan& P, const double2* four, int nf, int n_batch, double2* out,
+                      bool out_ext, cudaStream_t st);
+
+// fft.cu
+// Fourier rows [b][m][i] -> grid [b][i][j] (c2r, Im G_0 := 0), optional per-row 1/cos(phi).
+// Row b of the batch reads Fourier rows four[(b*in_stride + in_off)][m][i].
+void fft_rows_c2r(const pswe_plan& P, const double2* four, int in_stride, int in_off, double* grid, int n,
+                  bool div_cos, cudaStream_t st);
+// grid [b][i][j] -> Fourier rows [b][m][i], x pre (cos(phi) if pre_cos) then x post-scale:
+// mode 0: w_i/nlon (analyse), mode 1: w_i/(a cos^2 phi_i nlon) (vortdiv_from_uv).
+void fft_rows_r2c(const pswe_plan& P, const double* grid, double2* four, int out_stride, int out_off, int n,
+                  bool pre_cos, int scale_mode, double radius, cudaStream_t st);
+// Fused grid stage of eval_nonlinear (swe.cpp:41-54 + the FFT halves of uv_from_vortdiv /
+// synthesise / vortdiv_from_uv / analyse): four_in [b][4][m][i] (Phi, zeta, U, V) ->
+// four_out [b][5][m][i] (Phi'U, Phi'V, qU, qV, ke), weights folded in.
+void fft_eval_products(const pswe_plan& P, const pswe_params& prm, const double2* four_in,
+                       double2* four_out, int n_batch, cudaStream_t st);
+
+// ops.cu
+void eval_tail(const pswe_plan& P, const pswe_params& prm, const double2* proj, const double2* state,
+               double2* f_imp, double2* f_exp, int n_batch, cudaStream_t st);
+void vortdiv_tail(const pswe_plan& P, const double2* proj, double2* vort, double2* div, int n_pairs,
+                  cudaStream_t st);
+void eval_linear(int R, const pswe_params& prm, const double2* state, double2* out, int n_states,
+                 cudaStream_t st);
+void solve_implicit(int R, const pswe_params& prm, const double2* b, double c, double2* out,
+                    int n_states, cudaStream_t st);
+void laplacian(int R, const double2* x, double radius, double2* y, int n_fields, bool inverse,
+               cudaStream_t st);
+
+}  // namespace pswe
+
+namespace pswe {
+// SDC collocation tables (QuadratureTables, quadrature.hpp:16-22), row-major n x n.
+struct Tables {
+    int n = 0;
+    std::vector<double> nodes, q, qe, qi;  // row-major n x n
+    double Q(int i, int j) const { return q[(size_t)i * n + j]; }
+    double QE(int i, int j) const { return qe[(size_t)i * n + j]; }
+    double QI(int i, int j) const { return qi[(size_t)i * n + j]; }
+};
+
+Tables build_tables(int n);
+}  // namespace pswe
+
+// LevelSpec + SpaceTimeState (multilevel.hpp:16-23, sdc.hpp:14-20) on the device.
+struct pswe_level {
+    pswe_plan* plan = nullptr;
+    pswe_params prm{};
+    int R = 0, nn = 0;
+    long K = 0;
+    pswe::Tables tab;
+    double2* d_state = nullptr;  // [nn][3K]
+    double2* d_f[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [buffer][0=imp,1=exp] -> [nn][3K]
+    int cur = 0;
+    unsigned long long* d_res = nullptr;
+    double2* st(int node) const { return d_state + (size_t)node * 3 * K; }
+    double2* fi(int node, int buf = -1) const { return d_f[buf < 0 ? cur : buf][0] + (size_t)node * 3 * K; }
+    double2* fe(int node, int buf = -1) const { return d_f[buf < 0 ? cur : buf][1] + (size_t)node * 3 * K; }
+};
+
+struct pswe_pair {
+    pswe_level* fine = nullptr;
+    pswe_level* coarse = nullptr;
+    std::vector<double> tr, ti, qfr;  // (mc x mf), (mf x mc), (mc x mf)
+    double2* d_saved = nullptr;       // [3 families][mc][3Kc]
+    double2* saved(int fam, int node) const {
+        return d_saved + ((size_t)fam * coarse->nn + node) * 3 * coarse->K;
+    }
+};
+

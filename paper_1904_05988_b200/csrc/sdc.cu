@@ -1,0 +1,743 @@
+// SDC sweeper and two-level transfers on device-resident space-time states.
+//
+// Reference: sdc.cpp:7-72 (spread, refresh_node, sweep, collocation_residual, sdc_step),
+// quadrature.cpp:57-106 (tables), multilevel.cpp:9-158 (transfer matrices, restrict_states,
+// fas_correction, interpolate_increment, interpolate_states).
+//
+// Kernels:
+//   sweep_node_kernel   one SDC node update (sdc.cpp:31-46) fused with solve_implicit
+//                       (swe.cpp:77-98): reads up to 4(M+1)+2 node arrays, writes state[m+1].
+//   residual_kernel     collocation residual over all nodes, block max + atomicMax on the bit
+//                       pattern of a non-negative double (order-independent => deterministic).
+//   restrict/fas/interp coefficient gather kernels between the r-major triangles of Rf and Rc.
+// The node refresh is one batched eval_imex call (4 launches) for any number of nodes.
+#include <cmath>
+#include <cstring>
+
+#include "pswe_internal.h"
+
+namespace pswe {
+void eval_imex(pswe_plan& P, const pswe_params& prm, const double2* state, double2* f_imp, double2* f_exp, int n,
+               cudaStream_t st);
+
+// ---- quadrature tables (quadrature.cpp:19-106) ---------------------------------------------
+
+static std::vector<double> lobatto_nodes(int n) {
+    switch (n) {
+        case 2: return {0.0, 1.0};
+        case 3: return {0.0, 0.5, 1.0};
+        case 5: {
+            const double c = std::sqrt(3.0 / 7.0);
+            return {0.0, 0.5 * (1.0 - c), 0.5, 0.5 * (1.0 + c), 1.0};
+        }
+        default: throw std::invalid_argument("build_tables: supported node counts are 2, 3, 5");
+    }
+}
+
+double lagrange_basis(const std::vector<double>& nodes, int j, double x) {
+    double acc = 1.0;
+    for (int i = 0; i < (int)nodes.size(); ++i) {
+        if (i == j) continue;
+        acc *= (x - nodes[i]) / (nodes[j] - nodes[i]);
+    }
+    return acc;
+}
+
+static std::vector<double> lagrange_monomial(const std::vector<double>& nodes, int j) {
+    std::vector<double> c{1.0};
+    double denom = 1.0;
+    for (int i = 0; i < (int)nodes.size(); ++i) {
+        if (i == j) continue;
+        denom *= nodes[j] - nodes[i];
+        std::vector<double> next(c.size() + 1, 0.0);
+        for (size_t k = 0; k < c.size(); ++k) {
+            next[k] -= nodes[i] * c[k];
+            next[k + 1] += c[k];
+        }
+        c = std::move(next);
+    }
+    for (double& v : c) v /= denom;
+    return c;
+}
+
+static double integrate_monomial(const std::vector<double>& c, double upper) {
+    double acc = 0.0, xp = upper;
+    for (size_t k = 0; k < c.size(); ++k) {
+        acc += c[k] * xp / static_cast<double>(k + 1);
+        xp *= upper;
+    }
+    return acc;
+}
+
+Tables build_tables(int n) {
+    Tables t;
+    t.n = n;
+    t.nodes = lobatto_nodes(n);
+    t.q.assign((size_t)n * n, 0.0);
+    t.qe.assign((size_t)n * n, 0.0);
+    t.qi.assign((size_t)n * n, 0.0);
+    for (int j = 0; j < n; ++j) {
+        const auto c = lagrange_monomial(t.nodes, j);
+        for (int m = 0; m < n; ++m) t.q[(size_t)m * n + j] = integrate_monomial(c, t.nodes[m]);
+    }
+    for (int m = 1; m < n; ++m)
+        for (int j = 0; j < m; ++j) t.qe[(size_t)m * n + j] = t.nodes[j + 1] - t.nodes[j];
+    const int mm = n - 1;
+    std::vector<double> qt((size_t)mm * mm);
+    for (int i = 0; i < mm; ++i)
+        for (int j = 0; j < mm; ++j) qt[(size_t)i * mm + j] = t.q[(size_t)(1 + j) * n + 1 + i];
+    for (int k = 0; k < mm; ++k)
+        for (int i = k + 1; i < mm; ++i) {
+            const double l = qt[(size_t)i * mm + k] / qt[(size_t)k * mm + k];
+            for (int j = k; j < mm; ++j) qt[(size_t)i * mm + j] -= l * qt[(size_t)k * mm + j];
+        }
+    for (int i = 0; i < mm; ++i)
+        for (int j = 0; j <= i; ++j) t.qi[(size_t)(1 + i) * n + 1 + j] = qt[(size_t)j * mm + i];
+    return t;
+}
+
+// ---- kernels -------------------------------------------------------------------------------
+
+constexpr int kMaxNodes = 5;
+
+struct SweepNodeArgs {
+    const double2* theta0;
+    const double2* tau;  // tau[m+1] or nullptr
+    double2* out;
+    const double2* fe_new[kMaxNodes];
+    const double2* fe_old[kMaxNodes];
+    const double2* fi_new[kMaxNodes];
+    const double2* fi_old[kMaxNodes];
+    double ae[kMaxNodes], ai[kMaxNodes];  // dt*qE(m+1,j), dt*qI(m+1,j), j = 1..m
+    double aq[kMaxNodes];                 // dt*q(m+1,j), j = 0..M
+    double aii;                           // dt*qI(m+1,m+1)
+    int m, M, R;
+    double inv_a2, phi_bar, nu;
+};
+
+namespace {
+
+__device__ __forceinline__ void axpy(double2& acc, double a, double2 x) {
+    acc.x += a * x.x;
+    acc.y += a * x.y;
+}
+
+__device__ __forceinline__ int degree_of(int R, long k) {
+    const double b = 2.0 * R + 3.0;
+    int mm = (int)floor((b - sqrt(b * b - 8.0 * (double)k)) * 0.5);
+    if (mm < 0) mm = 0;
+    if (mm > R) mm = R;
+    while (mm > 0 && off_std(R, mm) > k) --mm;
+    while (mm < R && off_std(R, mm + 1) <= k) ++mm;
+    return mm + (int)(k - off_std(R, mm));
+}
+
+__device__ __forceinline__ void decode(int R, long k, int& m, int& s) {
+    s = degree_of(R, k);
+    const double b = 2.0 * R + 3.0;
+    int mm = (int)floor((b - sqrt(b * b - 8.0 * (double)k)) * 0.5);
+    if (mm < 0) mm = 0;
+    if (mm > R) mm = R;
+    while (mm > 0 && off_std(R, mm) > k) --mm;
+    while (mm < R && off_std(R, mm + 1) <= k) ++mm;
+    m = mm;
+    s = mm + (int)(k - off_std(R, mm));
+}
+
+// rhs (sdc.cpp:31-44, same axpy order) then solve_implicit (swe.cpp:77-98)
+__global__ void sweep_node_kernel(SweepNodeArgs A) {
+    const long K = (long)(A.R + 1) * (A.R + 2) / 2;
+    const long k = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    double2 r[3];
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+        const long i = f * K + k;
+        double2 acc = A.theta0[i];
+        for (int j = 1; j <= A.m; ++j) {
+            axpy(acc, A.ae[j], A.fe_new[j][i]);
+            axpy(acc, -A.ae[j], A.fe_old[j][i]);
+            axpy(acc, A.ai[j], A.fi_new[j][i]);
+            axpy(acc, -A.ai[j], A.fi_old[j][i]);
+        }
+        axpy(acc, -A.aii, A.fi_old[A.m + 1][i]);
+        for (int j = 0; j <= A.M; ++j) {
+            axpy(acc, A.aq[j], A.fi_old[j][i]);
+            axpy(acc, A.aq[j], A.fe_old[j][i]);
+        }
+        if (A.tau) {
+            const double2 t = A.tau[i];
+            acc.x += t.x;
+            acc.y += t.y;
+        }
+        r[f] = acc;
+    }
+    const int s = degree_of(A.R, k);
+    const double c = A.aii;
+    const double lam = -s * (s + 1.0) * A.inv_a2;
+    const double diff = 1.0 - c * A.nu * lam;
+    const double2 bp = make_double2(r[0].x / diff, r[0].y / diff);
+    const double2 bz = make_double2(r[1].x / diff, r[1].y / diff);
+    const double2 bd = make_double2(r[2].x / diff, r[2].y / diff);
+    const double ce = c / diff;
+    const double det = 1.0 - ce * ce * A.phi_bar * lam;
+    A.out[k] = make_double2((bp.x - ce * A.phi_bar * bd.x) / det, (bp.y - ce * A.phi_bar * bd.y) / det);
+    A.out[2 * K + k] = make_double2((bd.x - ce * lam * bp.x) / det, (bd.y - ce * lam * bp.y) / det);
+    A.out[K + k] = bz;
+}
+
+struct ResidualArgs {
+    const double2* state[kMaxNodes];
+    const double2* fi[kMaxNodes];
+    const double2* fe[kMaxNodes];
+    double w[kMaxNodes][kMaxNodes];  // -dt*q(m,j)
+    int nn;
+    long n3;  // 3K
+};
+
+__global__ void residual_kernel(ResidualArgs A, unsigned long long* out) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    double mx = 0.0;
+    if (i < A.n3) {
+        const double2 s0 = A.state[0][i];
+        for (int m = 0; m < A.nn; ++m) {
+            const double2 sm = A.state[m][i];
+            double2 acc = make_double2(sm.x - s0.x, sm.y - s0.y);
+            for (int j = 0; j < A.nn; ++j) {
+                axpy(acc, A.w[m][j], A.fi[j][i]);
+                axpy(acc, A.w[m][j], A.fe[j][i]);
+            }
+            mx = fmax(mx, hypot(acc.x, acc.y));
+        }
+    }
+    // block max
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ double wm[32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        mx = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(mx));
+    }
+}
+
+// coarse coefficient kc of a state (3 fields) -> fine coefficient index
+__device__ __forceinline__ long fine_index(int Rf, int Rc, long kc3, long Kc, long Kf) {
+    const int f = (int)(kc3 / Kc);
+    const long kc = kc3 - f * Kc;
+    int m, s;
+    decode(Rc, kc, m, s);
+    return f * Kf + off_std(Rf, m) + (s - m);
+}
+
+struct TimeMatArgs {
+    const double2* src[kMaxNodes];
+    const double2* src2[kMaxNodes];  // optional second operand (added / subtracted)
+    double w[kMaxNodes][kMaxNodes];
+    int rows, cols;
+};
+
+// y[i] = restrict( sum_j w(i,j) x[j] ) for every coarse node i (multilevel.cpp:100-107)
+__global__ void restrict_states_kernel(TimeMatArgs A, double2* const* __restrict__ dst_unused, double2* out0,
+                                       long stride_out, int Rf, int Rc) {
+    const long Kc = (long)(Rc + 1) * (Rc + 2) / 2, Kf = (long)(Rf + 1) * (Rf + 2) / 2;
+    const long kc3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (kc3 >= 3 * Kc) return;
+    const long kf3 = fine_index(Rf, Rc, kc3, Kc, Kf);
+    for (int i = 0; i < A.rows; ++i) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int j = 0; j < A.cols; ++j)
+            if (A.w[i][j] != 0.0) axpy(acc, A.w[i][j], A.src[j][kf3]);
+        out0[i * stride_out + kc3] = acc;
+    }
+}
+
+// tau_i = dt * [ restrict(sum_j qfr(i,j)(FI_f[j] + FE_f[j])) - sum_j qc(i,j)(FI_c[j] + FE_c[j]) ]
+// (multilevel.cpp:109-137, same operation order)
+struct FasArgs {
+    const double2* fi_f[kMaxNodes];
+    const double2* fe_f[kMaxNodes];
+    const double2* fi_c[kMaxNodes];
+    const double2* fe_c[kMaxNodes];
+    double qfr[kMaxNodes][kMaxNodes];
+    double qc[kMaxNodes][kMaxNodes];
+    int mc, mf, Rf, Rc;
+    double dt;
+};
+__global__ void fas_kernel(FasArgs A, double2* tau) {
+    const long Kc = (long)(A.Rc + 1) * (A.Rc + 2) / 2, Kf = (long)(A.Rf + 1) * (A.Rf + 2) / 2;
+    const long kc3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (kc3 >= 3 * Kc) return;
+    const long kf3 = fine_index(A.Rf, A.Rc, kc3, Kc, Kf);
+    for (int i = 0; i < A.mc; ++i) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int j = 0; j < A.mf; ++j) {
+            const double w = A.qfr[i][j];
+            if (w == 0.0) continue;
+            axpy(acc, w, A.fi_f[j][kf3]);
+            axpy(acc, w, A.fe_f[j][kf3]);
+        }
+        for (int j = 0; j < A.mc; ++j) {
+            const double w = A.qc[i][j];
+            if (w == 0.0) continue;
+            axpy(acc, -w, A.fi_c[j][kc3]);
+            axpy(acc, -w, A.fe_c[j][kc3]);
+        }
+        tau[i * 3 * Kc + kc3] = make_double2(acc.x * A.dt, acc.y * A.dt);
+    }
+}
+
+// fine[i] (+)= sum_j ti(i,j) pad(a[j] - b[j])  (interpolate_increment / interpolate_states,
+// multilevel.cpp:139-158). mode 0: add increments to 3 families (state, F_I, F_E);
+// mode 1: assign interpolated states.
+struct InterpArgs {
+    const double2* a[3][kMaxNodes];
+    const double2* b[3][kMaxNodes];  // saved (mode 0)
+    double2* dst[3][kMaxNodes];
+    double w[kMaxNodes][kMaxNodes];  // ti: (mf x mc)
+    int mf, mc, Rf, Rc, nfam;
+    double2* dstate0;  // optional: node-0 state increment (fine layout)
+};
+__global__ void interp_kernel(InterpArgs A, int mode) {
+    const long Kc = (long)(A.Rc + 1) * (A.Rc + 2) / 2, Kf = (long)(A.Rf + 1) * (A.Rf + 2) / 2;
+    const long kf3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (kf3 >= 3 * Kf) return;
+    const int f = (int)(kf3 / Kf);
+    const long kf = kf3 - f * Kf;
+    int m, s;
+    decode(A.Rf, kf, m, s);
+    const bool inside = (m <= A.Rc && s <= A.Rc);
+    const long kc3 = inside ? f * Kc + off_std(A.Rc, m) + (s - m) : 0;
+    for (int fam = 0; fam < A.nfam; ++fam) {
+        for (int i = 0; i < A.mf; ++i) {
+            double2 acc = make_double2(0.0, 0.0);
+            if (inside) {
+                for (int j = 0; j < A.mc; ++j) {
+                    const double w = A.w[i][j];
+                    if (w == 0.0) continue;
+                    double2 d = A.a[fam][j][kc3];
+                    if (mode == 0) {
+                        const double2 sv = A.b[fam][j][kc3];
+                        d = make_double2(d.x - sv.x, d.y - sv.y);
+                    }
+                    axpy(acc, w, d);
+                }
+            }
+            double2* o = A.dst[fam][i] + kf3;
+            if (mode == 0) {
+                const double2 cur = *o;
+                *o = make_double2(cur.x + acc.x, cur.y + acc.y);
+                if (fam == 0 && i == 0 && A.dstate0) A.dstate0[kf3] = acc;
+            } else {
+                *o = acc;
+            }
+        }
+    }
+}
+
+}  // namespace
+}  // namespace pswe
+
+using namespace pswe;
+
+namespace pswe {
+
+static void refresh(pswe_level* L, int first, int count, cudaStream_t st) {
+    if (count <= 0) return;
+    eval_imex(*L->plan, L->prm, L->st(first), L->fi(first), L->fe(first), count, st);
+}
+
+void level_spread(pswe_level* L, const double2* theta0, cudaStream_t st) {
+    const size_t bytes = 3 * L->K * sizeof(double2);
+    for (int m = 0; m < L->nn; ++m)
+        if (L->st(m) != theta0) PSWE_CUDA(cudaMemcpyAsync(L->st(m), theta0, bytes, cudaMemcpyDeviceToDevice, st));
+    refresh(L, 0, 1, st);
+    for (int m = 1; m < L->nn; ++m) {
+        PSWE_CUDA(cudaMemcpyAsync(L->fi(m), L->fi(0), bytes, cudaMemcpyDeviceToDevice, st));
+        PSWE_CUDA(cudaMemcpyAsync(L->fe(m), L->fe(0), bytes, cudaMemcpyDeviceToDevice, st));
+    }
+}
+
+void level_refresh(pswe_level* L, int first, int count, cudaStream_t st) { refresh(L, first, count, st); }
+
+void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) {
+    const int M = L->nn - 1;
+    const int old = L->cur, nw = 1 - L->cur;
+    const size_t bytes = 3 * L->K * sizeof(double2);
+    // node 0 keeps its right-hand sides (sdc.cpp:22-29: F_old is a copy; node 0 is not refreshed)
+    PSWE_CUDA(cudaMemcpyAsync(L->fi(0, nw), L->fi(0, old), bytes, cudaMemcpyDeviceToDevice, st));
+    PSWE_CUDA(cudaMemcpyAsync(L->fe(0, nw), L->fe(0, old), bytes, cudaMemcpyDeviceToDevice, st));
+    const Tables& t = L->tab;
+    for (int m = 0; m < M; ++m) {
+        SweepNodeArgs A{};
+        A.theta0 = L->st(0);
+        A.tau = tau ? tau + (size_t)(m + 1) * 3 * L->K : nullptr;
+        A.out = L->st(m + 1);
+        for (int j = 0; j <= M; ++j) {
+            A.fe_new[j] = L->fe(j, nw);
+            A.fi_new[j] = L->fi(j, nw);
+            A.fe_old[j] = L->fe(j, old);
+            A.fi_old[j] = L->fi(j, old);
+            A.aq[j] = dt * t.Q(m + 1, j);
+            if (j >= 1 && j <= m) {
+                A.ae[j] = dt * t.QE(m + 1, j);
+                A.ai[j] = dt * t.QI(m + 1, j);
+            }
+        }
+        A.aii = dt * t.QI(m + 1, m + 1);
+        A.m = m;
+        A.M = M;
+        A.R = L->R;
+        A.inv_a2 = 1.0 / (L->prm.radius * L->prm.radius);
+        A.phi_bar = L->prm.phi_bar;
+        A.nu = L->prm.nu;
+        const int bs = 128;
+        sweep_node_kernel<<<(unsigned)((L->K + bs - 1) / bs), bs, 0, st>>>(A);
+        PSWE_LAUNCH_CHECK();
+        eval_imex(*L->plan, L->prm, L->st(m + 1), L->fi(m + 1, nw), L->fe(m + 1, nw), 1, st);
+    }
+    L->cur = nw;
+}
+
+void level_residual(pswe_level* L, double dt, double* out, cudaStream_t st) {
+    ResidualArgs A{};
+    A.nn = L->nn;
+    A.n3 = 3 * L->K;
+    for (int m = 0; m < L->nn; ++m) {
+        A.state[m] = L->st(m);
+        A.fi[m] = L->fi(m);
+        A.fe[m] = L->fe(m);
+        for (int j = 0; j < L->nn; ++j) A.w[m][j] = -dt * L->tab.Q(m, j);
+    }
+    PSWE_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+    const int bs = 256;
+    residual_kernel<<<(unsigned)((A.n3 + bs - 1) / bs), bs, 0, st>>>(A, reinterpret_cast<unsigned long long*>(out));
+    PSWE_LAUNCH_CHECK();
+}
+
+void pair_restrict_states(pswe_pair* P, cudaStream_t st) {
+    pswe_level *F = P->fine, *C = P->coarse;
+    TimeMatArgs A{};
+    A.rows = C->nn;
+    A.cols = F->nn;
+    for (int j = 0; j < F->nn; ++j) A.src[j] = F->st(j);
+    for (int i = 0; i < C->nn; ++i)
+        for (int j = 0; j < F->nn; ++j) A.w[i][j] = P->tr[(size_t)i * F->nn + j];
+    const long n = 3 * C->K;
+    restrict_states_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(A, nullptr, C->st(0), 3 * C->K, F->R, C->R);
+    PSWE_LAUNCH_CHECK();
+}
+
+void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st) {
+    pswe_level *F = P->fine, *C = P->coarse;
+    FasArgs A{};
+    A.mc = C->nn;
+    A.mf = F->nn;
+    A.Rf = F->R;
+    A.Rc = C->R;
+    A.dt = dt;
+    for (int j = 0; j < F->nn; ++j) {
+        A.fi_f[j] = F->fi(j);
+        A.fe_f[j] = F->fe(j);
+    }
+    for (int j = 0; j < C->nn; ++j) {
+        A.fi_c[j] = C->fi(j);
+        A.fe_c[j] = C->fe(j);
+    }
+    for (int i = 0; i < C->nn; ++i) {
+        for (int j = 0; j < F->nn; ++j) A.qfr[i][j] = P->qfr[(size_t)i * F->nn + j];
+        for (int j = 0; j < C->nn; ++j) A.qc[i][j] = C->tab.Q(i, j);
+    }
+    const long n = 3 * C->K;
+    fas_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(A, tau);
+    PSWE_LAUNCH_CHECK();
+}
+
+void pair_save(pswe_pair* P, cudaStream_t st) {
+    pswe_level* C = P->coarse;
+    const size_t bytes = (size_t)C->nn * 3 * C->K * sizeof(double2);
+    PSWE_CUDA(cudaMemcpyAsync(P->saved(0, 0), C->st(0), bytes, cudaMemcpyDeviceToDevice, st));
+    PSWE_CUDA(cudaMemcpyAsync(P->saved(1, 0), C->fi(0), bytes, cudaMemcpyDeviceToDevice, st));
+    PSWE_CUDA(cudaMemcpyAsync(P->saved(2, 0), C->fe(0), bytes, cudaMemcpyDeviceToDevice, st));
+}
+
+void pair_interp_increment_add(pswe_pair* P, double2* dstate0, cudaStream_t st) {
+    pswe_level *F = P->fine, *C = P->coarse;
+    InterpArgs A{};
+    A.mf = F->nn;
+    A.mc = C->nn;
+    A.Rf = F->R;
+    A.Rc = C->R;
+    A.nfam = 3;
+    A.dstate0 = dstate0;
+    for (int j = 0; j < C->nn; ++j) {
+        A.a[0][j] = C->st(j);
+        A.a[1][j] = C->fi(j);
+        A.a[2][j] = C->fe(j);
+        for (int fam = 0; fam < 3; ++fam) A.b[fam][j] = P->saved(fam, j);
+    }
+    for (int i = 0; i < F->nn; ++i) {
+        A.dst[0][i] = F->st(i);
+        A.dst[1][i] = F->fi(i);
+        A.dst[2][i] = F->fe(i);
+        for (int j = 0; j < C->nn; ++j) A.w[i][j] = P->ti[(size_t)i * C->nn + j];
+    }
+    const long n = 3 * F->K;
+    interp_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(A, 0);
+    PSWE_LAUNCH_CHECK();
+}
+
+void pair_interp_states(pswe_pair* P, cudaStream_t st) {
+    pswe_level *F = P->fine, *C = P->coarse;
+    InterpArgs A{};
+    A.mf = F->nn;
+    A.mc = C->nn;
+    A.Rf = F->R;
+    A.Rc = C->R;
+    A.nfam = 1;
+    for (int j = 0; j < C->nn; ++j) A.a[0][j] = C->st(j);
+    for (int i = 0; i < F->nn; ++i) {
+        A.dst[0][i] = F->st(i);
+        for (int j = 0; j < C->nn; ++j) A.w[i][j] = P->ti[(size_t)i * C->nn + j];
+    }
+    const long n = 3 * F->K;
+    interp_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(A, 1);
+    PSWE_LAUNCH_CHECK();
+}
+
+// restrict_space / interpolate_space of n states
+__global__ void space_copy_kernel(int Rf, int Rc, const double2* __restrict__ x, double2* __restrict__ y, int down) {
+    const long Kc = (long)(Rc + 1) * (Rc + 2) / 2, Kf = (long)(Rf + 1) * (Rf + 2) / 2;
+    const int b = blockIdx.y;
+    if (down) {
+        const long kc3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+        if (kc3 >= 3 * Kc) return;
+        y[b * 3 * Kc + kc3] = x[b * 3 * Kf + fine_index(Rf, Rc, kc3, Kc, Kf)];
+    } else {
+        const long kf3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+        if (kf3 >= 3 * Kf) return;
+        const int f = (int)(kf3 / Kf);
+        int m, s;
+        decode(Rf, kf3 - f * Kf, m, s);
+        y[b * 3 * Kf + kf3] = (m <= Rc && s <= Rc) ? x[b * 3 * Kc + f * Kc + off_std(Rc, m) + (s - m)]
+                                                   : make_double2(0.0, 0.0);
+    }
+}
+
+}  // namespace pswe
+
+namespace {
+std::vector<double> lagrange_matrix(const std::vector<double>& from, const std::vector<double>& to) {
+    std::vector<double> pi(to.size() * from.size());
+    for (size_t i = 0; i < to.size(); ++i)
+        for (size_t j = 0; j < from.size(); ++j) pi[i * from.size() + j] = lagrange_basis(from, (int)j, to[i]);
+    return pi;
+}
+}  // namespace
+
+extern "C" {
+
+int pswe_quadrature_tables(int n, double* nodes, double* q, double* qe, double* qi) {
+    return guarded([&] {
+        const Tables t = build_tables(n);
+        std::memcpy(nodes, t.nodes.data(), sizeof(double) * n);
+        std::memcpy(q, t.q.data(), sizeof(double) * n * n);
+        std::memcpy(qe, t.qe.data(), sizeof(double) * n * n);
+        std::memcpy(qi, t.qi.data(), sizeof(double) * n * n);
+    });
+}
+
+int pswe_level_create(pswe_plan* plan, const pswe_params* p, int num_nodes, pswe_level** out) {
+    return guarded([&] {
+        if (!plan || !p || !out) throw std::invalid_argument("pswe_level_create: NULL argument");
+        auto* L = new pswe_level;
+        try {
+            L->plan = plan;
+            L->prm = *p;
+            L->R = plan->R;
+            L->K = plan->K;
+            L->nn = num_nodes;
+            L->tab = build_tables(num_nodes);
+            const size_t bytes = (size_t)num_nodes * 3 * L->K * sizeof(double2);
+            PSWE_CUDA(cudaMalloc(&L->d_state, bytes));
+            for (int b = 0; b < 2; ++b)
+                for (int k = 0; k < 2; ++k) PSWE_CUDA(cudaMalloc(&L->d_f[b][k], bytes));
+            PSWE_CUDA(cudaMemset(L->d_state, 0, bytes));
+            plan->reserve(num_nodes);
+        } catch (...) {
+            if (L->d_state) cudaFree(L->d_state);
+            for (auto& b : L->d_f)
+                for (auto* q : b)
+                    if (q) cudaFree(q);
+            delete L;
+            throw;
+        }
+        *out = L;
+    });
+}
+
+int pswe_level_destroy(pswe_level* L) {
+    return guarded([&] {
+        if (!L) return;
+        cudaFree(L->d_state);
+        for (auto& b : L->d_f)
+            for (auto* q : b) cudaFree(q);
+        delete L;
+    });
+}
+
+double* pswe_level_ptr(pswe_level* L, int which, int node) {
+    if (!L || node < 0 || node >= L->nn) return nullptr;
+    switch (which) {
+        case 0: return reinterpret_cast<double*>(L->st(node));
+        case 1: return reinterpret_cast<double*>(L->fi(node));
+        case 2: return reinterpret_cast<double*>(L->fe(node));
+        default: return nullptr;
+    }
+}
+
+int pswe_level_info(const pswe_level* L, int* R, int* nn) {
+    return guarded([&] {
+        if (!L) throw std::invalid_argument("NULL level");
+        if (R) *R = L->R;
+        if (nn) *nn = L->nn;
+    });
+}
+
+int pswe_spread(pswe_level* L, const double* theta0, void* stream) {
+    return guarded([&] {
+        if (!L || !theta0) throw std::invalid_argument("pswe_spread: NULL argument");
+        level_spread(L, reinterpret_cast<const double2*>(theta0), as_stream(stream));
+    });
+}
+
+int pswe_refresh_nodes(pswe_level* L, int first, int count, void* stream) {
+    return guarded([&] {
+        if (!L) throw std::invalid_argument("NULL level");
+        if (first < 0 || count < 0 || first + count > L->nn) throw std::invalid_argument("refresh: node range");
+        level_refresh(L, first, count, as_stream(stream));
+    });
+}
+
+int pswe_sweep(pswe_level* L, double dt, const double* tau, void* stream) {
+    return guarded([&] {
+        if (!L) throw std::invalid_argument("NULL level");
+        level_sweep(L, dt, reinterpret_cast<const double2*>(tau), as_stream(stream));
+    });
+}
+
+int pswe_collocation_residual(pswe_level* L, double dt, double* out, void* stream) {
+    return guarded([&] {
+        if (!L || !out) throw std::invalid_argument("NULL argument");
+        level_residual(L, dt, out, as_stream(stream));
+    });
+}
+
+int pswe_sdc_step(pswe_level* L, const double* theta0, double dt, int n_sweeps, double* out_res, void* stream) {
+    return guarded([&] {
+        if (!L || !theta0) throw std::invalid_argument("NULL argument");
+        const cudaStream_t st = as_stream(stream);
+        level_spread(L, reinterpret_cast<const double2*>(theta0), st);
+        for (int k = 0; k < n_sweeps; ++k) level_sweep(L, dt, nullptr, st);
+        if (out_res) level_residual(L, dt, out_res, st);
+    });
+}
+
+int pswe_pair_create(pswe_level* fine, pswe_level* coarse, pswe_pair** out) {
+    return guarded([&] {
+        if (!fine || !coarse || !out) throw std::invalid_argument("pswe_pair_create: NULL argument");
+        if (coarse->R > fine->R) throw std::invalid_argument("make_transfer_pair: coarse truncation exceeds fine");
+        if (coarse->R < 1) throw std::invalid_argument("make_transfer_pair: coarse truncation must be >= 1");
+        const int nf = fine->nn, nc = coarse->nn;
+        if (!(nf == nc || (nf == 3 && nc == 2) || (nf == 5 && nc == 3)))
+            throw std::invalid_argument("make_transfer_pair: unsupported node pair");
+        auto* P = new pswe_pair;
+        P->fine = fine;
+        P->coarse = coarse;
+        P->tr = lagrange_matrix(fine->tab.nodes, coarse->tab.nodes);
+        P->ti = lagrange_matrix(coarse->tab.nodes, fine->tab.nodes);
+        // matmul (quadrature.cpp:8-17), i-k-j order
+        P->qfr.assign((size_t)nc * nf, 0.0);
+        for (int i = 0; i < nc; ++i)
+            for (int k = 0; k < nf; ++k) {
+                const double xv = P->tr[(size_t)i * nf + k];
+                for (int j = 0; j < nf; ++j) P->qfr[(size_t)i * nf + j] += xv * fine->tab.Q(k, j);
+            }
+        const size_t bytes = (size_t)3 * nc * 3 * coarse->K * sizeof(double2);
+        try {
+            PSWE_CUDA(cudaMalloc(&P->d_saved, bytes));
+        } catch (...) {
+            delete P;
+            throw;
+        }
+        *out = P;
+    });
+}
+
+int pswe_pair_destroy(pswe_pair* P) {
+    return guarded([&] {
+        if (!P) return;
+        cudaFree(P->d_saved);
+        delete P;
+    });
+}
+
+int pswe_restrict_space(int rf, int rc, const double* x, double* y, int n, void* stream) {
+    return guarded([&] {
+        if (rc > rf || rc < 1) throw std::invalid_argument("restrict_space: bad truncations");
+        if (n <= 0) return;
+        const long Kc = num_coeffs(rc);
+        space_copy_kernel<<<dim3((unsigned)((3 * Kc + 127) / 128), n), 128, 0, as_stream(stream)>>>(
+            rf, rc, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), 1);
+        PSWE_LAUNCH_CHECK();
+    });
+}
+
+int pswe_interpolate_space(int rc, int rf, const double* x, double* y, int n, void* stream) {
+    return guarded([&] {
+        if (rc > rf || rc < 1) throw std::invalid_argument("interpolate_space: bad truncations");
+        if (n <= 0) return;
+        const long Kf = num_coeffs(rf);
+        space_copy_kernel<<<dim3((unsigned)((3 * Kf + 127) / 128), n), 128, 0, as_stream(stream)>>>(
+            rf, rc, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), 0);
+        PSWE_LAUNCH_CHECK();
+    });
+}
+
+int pswe_restrict_states(pswe_pair* P, void* stream) {
+    return guarded([&] {
+        if (!P) throw std::invalid_argument("NULL pair");
+        pair_restrict_states(P, as_stream(stream));
+    });
+}
+
+int pswe_fas_correction(pswe_pair* P, double dt, double* tau, void* stream) {
+    return guarded([&] {
+        if (!P || !tau) throw std::invalid_argument("NULL argument");
+        pair_fas(P, dt, reinterpret_cast<double2*>(tau), as_stream(stream));
+    });
+}
+
+int pswe_save_coarse(pswe_pair* P, void* stream) {
+    return guarded([&] {
+        if (!P) throw std::invalid_argument("NULL pair");
+        pair_save(P, as_stream(stream));
+    });
+}
+
+int pswe_interpolate_increment_add(pswe_pair* P, double* dstate0, void* stream) {
+    return guarded([&] {
+        if (!P) throw std::invalid_argument("NULL pair");
+        pair_interp_increment_add(P, reinterpret_cast<double2*>(dstate0), as_stream(stream));
+    });
+}
+
+int pswe_interpolate_states(pswe_pair* P, void* stream) {
+    return guarded([&] {
+        if (!P) throw std::invalid_argument("NULL pair");
+        pair_interp_states(P, as_stream(stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,123 @@
+"""GPU parity of the SWE right-hand side (swe.cpp) against the reference's outputs
+(tests/golden) and the numpy oracle, plus the reference's property tests (test_swe.cpp)."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from _util import rel_diff_fields  # noqa: E402
+from oracle import fixtures as fx  # noqa: E402
+from oracle import pswe_oracle as O  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1904_05988_b200 as P
+    return P
+
+
+def cuda(a):
+    return torch.as_tensor(np.asarray(a)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("tag,R", [("t15", 15), ("t31", 31), ("t31lin", 31)])
+def test_operators_vs_reference(P, golden, tag, R, mode):
+    nlat, nlon = (int(v) for v in golden[f"{tag}_grid"])
+    plan = P.TransformPlan(R, nlat, nlon, mode)
+    p = P.ModelParams(nu=1e5)
+    st = cuda(golden[f"swe_{tag}_state"])
+    assert rel_diff_fields(host(P.eval_linear(R, st, p)), golden[f"swe_{tag}_lin"]) < 1e-14
+    assert rel_diff_fields(host(P.solve_implicit(R, st, 50.0, p)), golden[f"swe_{tag}_solve"]) < 1e-14
+    assert rel_diff_fields(host(P.eval_nonlinear(st, p, plan)), golden[f"swe_{tag}_nonlin"]) < 1e-11
+    rough = cuda(golden[f"swe_{tag}_rough"])
+    assert rel_diff_fields(host(P.eval_nonlinear(rough, p, plan)), golden[f"swe_{tag}_rough_nonlin"]) < 1e-11
+    fi, fe = P.imex_split(st, p, plan)
+    assert rel_diff_fields(host(fi), golden[f"swe_{tag}_lin"]) < 1e-14
+    assert rel_diff_fields(host(fe), golden[f"swe_{tag}_nonlin"]) < 1e-11
+
+
+@pytest.mark.parametrize("R,grid", [(63, (96, 192)), (255, (256, 512))])
+def test_eval_vs_numpy_oracle(P, R, grid):
+    """eval_nonlinear at T63 (reference grid) and T255 on BASELINE's 256x512 grid."""
+    plan = P.TransformPlan(R, grid[0], grid[1])
+    ref = O.TransformPlan(R, grid[0], grid[1])
+    p = P.ModelParams(phi_bar=9.80616 * 1e4)
+    st = fx.random_state(R, 5, 1e3, 1e-5)
+    _, ss = fx.degree_order(R)
+    st *= (ss + 1.0) ** -1.5
+    st[0, 0] = p.phi_bar * math.sqrt(2.0)
+    st[1:, 0] = 0
+    po = O.ModelParams(phi_bar=p.phi_bar)
+    mine = host(P.eval_nonlinear(cuda(st), p, plan))
+    assert rel_diff_fields(mine, O.eval_nonlinear(st, po, ref)) < 1e-11
+
+
+def test_batched_equals_single(P):
+    R = 31
+    plan = P.TransformPlan(R)
+    p = P.ModelParams(nu=1e5)
+    sts = np.stack([fx.smooth_state(R, p.phi_bar, s) for s in range(5)])
+    batch = host(P.imex_split(cuda(sts), p, plan)[1])
+    for i in range(5):
+        single = host(P.eval_nonlinear(cuda(sts[i]), p, plan))
+        np.testing.assert_array_equal(batch[i], single)
+
+
+def test_nonlinear_properties(P):
+    """test_swe.cpp:75-129."""
+    R = 15
+    plan = P.TransformPlan(R)
+    p = P.ModelParams(nu=1e5)
+    s = np.zeros((3, P.num_coeffs(R)), dtype=np.complex128)
+    s[0] = fx.random_field(R, 5) * 1e3
+    s[0, 0] += p.phi_bar * math.sqrt(2)
+    out = host(P.eval_nonlinear(cuda(s), p, plan))
+    assert np.abs(out).max() < 1e-12 * np.abs(s[0]).max()
+    sm = fx.smooth_state(R, p.phi_bar, 17)
+    nl = host(P.eval_nonlinear(cuda(sm), p, plan))
+    li = host(P.eval_linear(R, cuda(sm), p))
+    assert nl[0, 0] == 0 and nl[2, 0] == 0 and li[0, 0] == 0 and li[2, 0] == 0
+    s = np.stack([fx.random_field(R, 31), fx.random_field(R, 32), fx.random_field(R, 33)])
+    _, ss = fx.degree_order(R)
+    decay = np.exp(-((ss / 3.0) ** 2))
+    s[0] *= decay
+    s[1] *= 1e-6 * decay
+    s[2] *= 1e-6 * decay
+    s[1, 0] = s[2, 0] = 0
+    # test_swe.cpp:370-377 keeps the default phi_bar, so Phi' = Phi - phi_bar is dominated by
+    # -phi_bar and the flux is LINEAR in the winds: the reference's own code gives ratio 2.0000005
+    # there (checked with oracle/_ref), i.e. that reference test cannot pass as written. We check
+    # the reference's value, and the intended quadratic property with phi_bar = 0.
+    q = P.ModelParams(omega=0.0, nu=0.0)
+    n1 = np.abs(host(P.eval_nonlinear(cuda(s), q, plan))[0]).max()
+    n2 = np.abs(host(P.eval_nonlinear(cuda(0.5 * s), q, plan))[0]).max()
+    assert abs(n1 / n2 - 2.0000004845649686) < 1e-9
+    q = P.ModelParams(omega=0.0, nu=0.0, phi_bar=0.0)
+    n1 = np.abs(host(P.eval_nonlinear(cuda(s), q, plan))[0]).max()
+    n2 = np.abs(host(P.eval_nonlinear(cuda(0.5 * s), q, plan))[0]).max()
+    assert abs(n1 / n2 - 4.0) < 1e-9
+
+
+def test_implicit_solve_residual(P):
+    """test_swe.cpp:131-170."""
+    R = 10
+    for nu in (0.0, 1.0):
+        p = P.ModelParams(radius=1.0, omega=1.0, gravity=1.0, phi_bar=1.0, nu=nu)
+        for c in (1e-3, 0.3, 1.0, 1e3):
+            b = cuda(fx.random_state(R, 7 + int(c * 10)))
+            x = P.solve_implicit(R, b, c, p)
+            res = host(x - c * P.eval_linear(R, x, p) - b)
+            assert np.abs(res).max() < 1e-12 * np.abs(host(b)).max()
+    p = P.ModelParams(radius=1.0, omega=1.0, gravity=1.0, phi_bar=1.0, nu=1.0)
+    b = np.zeros((3, P.num_coeffs(R)), dtype=np.complex128)
+    b[1, O.index(R, 0, 2)] = 1.0
+    x = host(P.solve_implicit(R, cuda(b), 1.0, p))
+    assert abs(x[1, O.index(R, 0, 2)].real - 1.0 / 7.0) < 1e-15
