@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark of the PFASST-SH hot path on B200.
+
+Headline metric (BASELINE.json): SWE RHS evals/s (fp64 SH fwd+inv) at T255.
+  step  = one explicit+implicit right-hand-side evaluation (eval_nonlinear + eval_linear,
+          swe.cpp:9-69) of B = 5 T255 states (the 5 fine SDC nodes of config 3; refresh of all
+          nodes after prediction/restriction), on the reference's own T255 grid 384 x 768.
+  value = evals/s over the whole job (all ranks; each rank evaluates its own states: weak).
+  L2    = flushed (256 MiB write) between timed steps, outside the event-timed span.
+Side results on the same JSON line:
+  e2e            same metric through the public API with pinned HOST buffers, H2D + D2H inside
+                 the timed region;
+  roofline       dominant kernel's algorithmic FP64 flops / its event-timed duration vs the
+                 FP64 peak measured in-run (MEASURED_PEAKS.json has no FP64 figure);
+  cpu_baseline   the reference (oracle/_ref, compiled from /root/reference) timed on the host
+                 cores, rank 0 at N=1 only;
+  pfasst         config-3-shape PFASST block (T255/T127, 5/3 nodes, dt 60 s, 8 steps, 4 its),
+                 n_ts = N time ranks (NCCL) — wall s per simulated day;
+  transform      config-2 micro-bench: 15-field round trip at T255 on 256 x 512.
+--impl reference times the reference's CPU path (oracle/_ref) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SWE RHS evals/s (fp64 SH fwd+inv) at T255"
+R_BENCH, NLAT, NLON, BATCH = 255, 384, 768, 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-pfasst", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--legendre", type=int, default=0, help="0 recompute, 1 stream")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def bench_states(R=R_BENCH, n=BATCH, seed=20261019):
+    from paper_1904_05988_b200.cases import balanced_random_state
+    return np.stack([balanced_random_state(R, 40.0, seed + i) for i in range(n)])
+
+
+# ----------------------------------------------------------------------------------------------
+# reference arm / CPU baseline (oracle/_ref = the reference C++ compiled from its own sources)
+
+
+def reference_eval_rate(seconds: float, threads: int | None = None):
+    from oracle import ref_lib as ref
+    from oracle.pswe_oracle import ModelParams
+    if threads:
+        ref.lib().ref_set_threads(threads)
+    cores = ref.lib().ref_max_threads()
+    plan = ref.RefPlan(R_BENCH)  # reference dealiased grid 384 x 768
+    st = bench_states(n=1)[0]
+    p = ModelParams(phi_bar=9.80616 * 1e4)
+    ref.lib()  # noqa
+    plan.time_eval(st, p, 1)  # warm
+    n, t0 = 0, time.perf_counter()
+    while True:
+        plan.time_eval(st, p, 1)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return n / el, cores, f"{n} sequential eval_nonlinear+eval_linear calls at T255 384x768 ({el:.1f} s)"
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import ref_lib as ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpintswe_ref.so not built"}))
+        return
+    from oracle.pswe_oracle import ModelParams
+    plan = ref.RefPlan(R_BENCH)
+    states = bench_states()
+    p = ModelParams(phi_bar=9.80616 * 1e4)
+    cores = ref.lib().ref_max_threads()
+
+    def step():
+        for s in states:
+            plan.time_eval(s, p, 1)
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = BATCH * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded balanced n^-3 random states, 40 m/s rms)",
+        "config": {"workload": f"rhs_eval T{R_BENCH} {NLAT}x{NLON} x{BATCH} states", "R": R_BENCH, "nlat": NLAT,
+                   "nlon": NLON, "batch_states": BATCH},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} steps x {BATCH} evals, reference eval_nonlinear+eval_linear "
+                                   f"(OpenMP {cores} threads, FFTW-API shim)"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------------------------
+# clocks sampler
+
+
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(dev)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons, pw = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+                pw.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        busy = [s for s in sm if mx and s > 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+# ----------------------------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1904_05988_b200 as P
+    from paper_1904_05988_b200 import _lib
+    from paper_1904_05988_b200.transform import _stream
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    L = _lib.lib()
+
+    prm = P.ModelParams(phi_bar=9.80616 * 1e4)
+    cprm = prm.c()
+    plan = P.TransformPlan(R_BENCH, NLAT, NLON, args.legendre)
+    plan.reserve(BATCH)
+    states = torch.as_tensor(bench_states()).to(dev)
+    fi = torch.empty_like(states)
+    fe = torch.empty_like(states)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def step():
+        _lib.check(L.pswe_eval_imex(plan.handle, ctypes.byref(cprm), states.data_ptr(), fi.data_ptr(),
+                                    fe.data_ptr(), BATCH, _stream()))
+
+    clocks = Clocks(local)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.zero_()
+        ev0[k].record()
+        step()
+        ev1[k].record()
+    torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    torch.cuda.synchronize()
+    value = world * BATCH * args.steps / (total_ms * 1e-3)
+    gpu_launches = 4 * args.steps
+
+    # per-kernel durations (same workload, L2 flushed) for the roofline
+    stage = np.zeros(4)
+    ms4 = (ctypes.c_float * 4)()
+    for k in range(args.steps):
+        flush.zero_()
+        _lib.check(L.pswe_eval_imex_timed(plan.handle, ctypes.byref(cprm), states.data_ptr(), fi.data_ptr(),
+                                          fe.data_ptr(), BATCH, _stream(), ms4))
+        stage += np.array(list(ms4))
+    stage /= args.steps
+    J = NLAT // 2
+    F_L = NLAT * (R_BENCH + 1) * (R_BENCH + 2)  # flops per complex field per direction
+    nlog = math.log2(NLON)
+    fft_flops = 2.5 * NLAT * NLON * nlog  # per real row-field per direction
+    algo = {
+        "legendre_inverse": 4 * BATCH * F_L,            # Phi, zeta, U, V
+        "fft_products": 9 * BATCH * fft_flops + 15.0 * BATCH * NLAT * NLON,
+        "legendre_forward": 5 * BATCH * F_L,            # Phi'U, Phi'V, qU, qV, ke
+        "tail": 30.0 * BATCH * P.num_coeffs(R_BENCH),
+    }
+    names = list(algo)
+    dom = names[int(np.argmax(stage))]
+    peak_dfma = float(L.pswe_fp64_peak(0, 4096))
+    peak_dmma = float(L.pswe_fp64_peak(1, 2048))
+    achieved = algo[dom] / (stage[names.index(dom)] * 1e-3) / 1e12
+    peak = max(peak_dfma, peak_dmma)
+    roofline = {
+        "bound": "tensor", "pipe": "fp64", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak, "traffic": None,
+        "peak_source": f"measured in-run FP64 microbenchmarks (DFMA {peak_dfma:.1f}, DMMA m8n8k4 {peak_dmma:.1f} "
+                       f"TFLOP/s); MEASURED_PEAKS.json has no FP64 figure",
+        "algorithmic_flops_per_launch": algo[dom],
+        "stage_ms": {n: float(v) for n, v in zip(names, stage)},
+        "stage_frac_of_fp64_peak": {n: algo[n] / (v * 1e-3) / 1e12 / peak for n, v in zip(names, stage)},
+    }
+
+    # e2e through the public API with pinned host buffers
+    h_in = torch.as_tensor(bench_states()).pin_memory()
+    h_fi = torch.empty_like(h_in).pin_memory()
+    h_fe = torch.empty_like(h_in).pin_memory()
+    d_in = torch.empty_like(states)
+
+    def e2e_step():
+        d_in.copy_(h_in, non_blocking=True)
+        a, b = P.imex_split(d_in, prm, plan)
+        h_fi.copy_(a, non_blocking=True)
+        h_fe.copy_(b, non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    st_bytes = BATCH * 3 * P.num_coeffs(R_BENCH) * 16
+    e2e = {"value": world * BATCH * args.steps / (e2e_ms * 1e-3), "unit": "evals/s",
+           "h2d_bytes_per_step": st_bytes, "d2h_bytes_per_step": 2 * st_bytes}
+
+    # config-2 transform micro-bench (15 fields, T255, 256x512)
+    tplan = P.TransformPlan(255, 256, 512, args.legendre)
+    tplan.reserve(3)
+    rng = np.random.default_rng(2)
+    rs = np.concatenate([np.full(256 - r, r) for r in range(256)])
+    ss = np.concatenate([np.arange(r, 256) for r in range(256)])
+    x = (rng.uniform(-1, 1, (15, rs.size)) + 1j * rng.uniform(-1, 1, (15, rs.size))) * (ss + 1.0) ** -1.5
+    x[:, rs == 0] = x[:, rs == 0].real
+    xd = torch.as_tensor(x).to(dev)
+    g = torch.empty((15, 256, 512), dtype=torch.float64, device=dev)
+    xb = torch.empty_like(xd)
+
+    def rt():
+        _lib.check(L.pswe_synthesise(tplan.handle, xd.data_ptr(), g.data_ptr(), 15, _stream()))
+        _lib.check(L.pswe_analyse(tplan.handle, g.data_ptr(), xb.data_ptr(), 15, _stream()))
+
+    for _ in range(3):
+        rt()
+    tms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        rt()
+        b.record()
+        torch.cuda.synchronize()
+        tms += a.elapsed_time(b)
+    tms /= args.steps
+    rt_err = float((xb - xd).abs().max() / xd.abs().max())
+    F_L2 = 256 * 256 * 257
+    rt_flops = 2 * 15 * F_L2 + 2 * 15 * 2.5 * 256 * 512 * 9
+    transform = {"workload": "config 2: 15 fields T255 256x512 synthesise+analyse", "us_per_roundtrip": 1e3 * tms,
+                 "roundtrip_rel_err": rt_err, "tflops": rt_flops / (tms * 1e-3) / 1e12,
+                 "frac_of_fp64_peak": rt_flops / (tms * 1e-3) / 1e12 / peak}
+
+    # PFASST (config-3 shape) at n_ts = world
+    pf_res = None
+    if not args.no_pfasst:
+        try:
+            pf_res = run_pfasst(P, prm, world, rank, dev, clocks_dev=local)
+        except Exception as e:  # reported, never hides the headline
+            pf_res = {"error": f"{type(e).__name__}: {e}"}
+
+    clk = clocks.stop()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, cores, sample = reference_eval_rate(10.0)
+            cpu = {"value": v, "unit": "evals/s", "cores": cores, "kind": "reference", "sample": sample}
+        except Exception as e:
+            cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded balanced n^-3 random states, 40 m/s rms; BASELINE config shapes)",
+            "config": {"workload": f"rhs_eval T{R_BENCH} {NLAT}x{NLON} x{BATCH} states per rank per step",
+                       "R": R_BENCH, "nlat": NLAT, "nlon": NLON, "batch_states": BATCH,
+                       "legendre": "recompute" if args.legendre == 0 else "stream",
+                       "l2": "flushed between timed steps (256 MiB write, outside the timed span)",
+                       "parallelism": f"{world} rank(s), independent states per rank"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": gpu_launches,
+            "transform": transform, "pfasst": pf_res,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_pfasst(P, prm, world, rank, dev, clocks_dev=0):
+    """Config-3 shape: T255 (384x768) / T127 (192x384), 5/3 nodes, dt 60 s, 8 steps, 4 its."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1904_05988_b200.cases import config_state
+    steps, dt, n_iter = 8, 60.0, 4
+    if steps % world:
+        return {"skipped": f"8 steps not divisible by {world} ranks"}
+    n_blocks = steps // world
+    pf_plan = P.TransformPlan(255)
+    pc_plan = P.TransformPlan(127)
+    fine, coarse = P.Level(pf_plan, prm, 5), P.Level(pc_plan, prm, 3)
+    pair = P.TransferPair(fine, coarse)
+    cfg = P.BlockConfig(world, dt, n_iter)
+    if world == 1:
+        pf = P.Pfasst(pair, cfg)
+    else:
+        uid = [P.pfasst.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        pf = P.Pfasst(pair, cfg, rank=rank, world=world, nccl_id=uid[0])
+    theta0 = torch.as_tensor(config_state(3, pf_plan)).to(dev)
+    P.run_blocks(pf, theta0, 1)  # warm-up block
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    fin, hist = P.run_blocks(pf, theta0, n_blocks)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    wall = ms * 1e-3
+    return {"config": "config 3 shape: T255(384x768)/T127(192x384), 5/3 nodes, dt 60 s, 8 steps, 4 iterations",
+            "n_ts": world, "blocks": n_blocks, "wall_s": wall, "wall_s_per_sim_day": wall / (steps * dt) * 86400,
+            "final_residuals": [float(r) for r in hist[-1][:, -1]]}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
