@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(64) leg_inv_kernel(int R, int J, int nlat, con
 #pragma unroll
         for (int f = 0; f < NF; ++f) cfma(aE[f], coef[f * len + t], p);
     }
-    const int iN = nlat / 2 + j, iS = nlat / 2 - 1 - j;
+    const int iN = nlat - J + j, iS = J - 1 - j;  // iN == iS: equator (odd nlat)
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
         double2* o = out + (((long)b * NF + f) * (R + 1) + m) * nlat;
@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(64) leg_fwd_stream_kernel(int R, int J, int nl
     for (int idx = threadIdx.x; idx < NF * J; idx += blockDim.x) {
         const int f = idx / J, j = idx - f * J;
         const double2* src = four + (((long)b * nf + f0 + f) * (R + 1) + m) * nlat;
-        const double2 gn = src[nlat / 2 + j], gs = src[nlat / 2 - 1 - j];
+        const int iN = nlat - J + j, iS = J - 1 - j;
+        const double2 gn = src[iN], gs = (iN == iS) ? make_double2(0.0, 0.0) : src[iS];
         g[(2 * f) * J + j] = make_double2(gn.x + gs.x, gn.y + gs.y);
         g[(2 * f + 1) * J + j] = make_double2(gn.x - gs.x, gn.y - gs.y);
     }
@@ -233,7 +234,8 @@ __global__ void __launch_bounds__(256) leg_fwd_rec_kernel(int R, int J, int nlat
     for (int idx = threadIdx.x; idx < NF * J; idx += NT) {
         const int f = idx / J, j = idx - f * J;
         const double2* src = four + (((long)b * nf + f0 + f) * (R + 1) + m) * nlat;
-        const double2 gn = src[nlat / 2 + j], gs = src[nlat / 2 - 1 - j];
+        const int iN = nlat - J + j, iS = J - 1 - j;
+        const double2 gn = src[iN], gs = (iN == iS) ? make_double2(0.0, 0.0) : src[iS];
         g[(2 * f) * J + j] = make_double2(gn.x + gs.x, gn.y + gs.y);
         g[(2 * f + 1) * J + j] = make_double2(gn.x - gs.x, gn.y - gs.y);
     }
@@ -310,6 +312,11 @@ __global__ void __launch_bounds__(256) leg_fwd_rec_kernel(int R, int J, int nlat
 void legendre_inverse(const pswe_plan& P, int kind, const double2* in, const double2* in2, int n, double radius,
                       double2* out, cudaStream_t st) {
     if (n <= 0) return;
+    if (!P.simt) {  // default: FP64 tensor cores (legendre_mma.cu)
+        const int nq = n * (kind == INV_PLAIN ? 1 : kind == INV_UV ? 2 : 4);
+        legendre_inverse_mma(P, kind, in, in2, nq, radius, out, st);
+        return;
+    }
     const int TJ = 64;
     const int len = P.R + 2;
     auto launch = [&](auto kern, int nf, int nz) {
@@ -370,6 +377,8 @@ void legendre_forward(const pswe_plan& P, const double2* four, int nf, int n_bat
         if (nf % 5 == 0) fwd_stream<5>(P, four, nf, n_batch, out, ext, st);
         else if (nf % 2 == 0) fwd_stream<2>(P, four, nf, n_batch, out, ext, st);
         else fwd_stream<1>(P, four, nf, n_batch, out, ext, st);
+    } else if (!P.simt) {  // default: FP64 tensor cores (legendre_mma.cu)
+        legendre_forward_mma(P, four, nf * n_batch, out, ext, st);
     } else {
         // shared-memory budget: g = NF*2*J*16 B, tile = J*SC*8 B
         if (nf % 5 == 0 && P.J <= 384) fwd_rec<5, 32>(P, four, nf, n_batch, out, ext, st);

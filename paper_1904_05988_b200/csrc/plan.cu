@@ -8,6 +8,7 @@
 //   dealiased_nlon   transform.cpp:38-43
 // Device tables are laid out for the kernels.
 #include <cmath>
+#include <cstdlib>
 #include <complex>
 #include <cstring>
 #include <mutex>
@@ -127,17 +128,20 @@ void pswe_plan::reserve(int batch) {
     if (d_four_a) cudaFree(d_four_a);
     if (d_four_b) cudaFree(d_four_b);
     if (d_proj) cudaFree(d_proj);
-    d_four_a = d_four_b = d_proj = nullptr;
+    if (d_xcoef) cudaFree(d_xcoef);
+    d_four_a = d_four_b = d_proj = d_xcoef = nullptr;
     const size_t four = (size_t)batch * 5 * (R + 1) * nlat;
     PSWE_CUDA(cudaMalloc(&d_four_a, four * sizeof(double2)));
     PSWE_CUDA(cudaMalloc(&d_four_b, four * sizeof(double2)));
     PSWE_CUDA(cudaMalloc(&d_proj, (size_t)batch * 5 * Kx * sizeof(double2)));
+    PSWE_CUDA(cudaMalloc(&d_xcoef, (size_t)batch * 5 * Kx * sizeof(double2)));
     cap_batch = batch;
 }
 
 static void plan_free(pswe_plan* p) {
     void* ptrs[] = {p->d_mu_n, p->d_seed, p->d_rec, p->d_eps, p->d_ptab, p->d_rowc, p->d_roww,
-                    p->d_rowmu, p->d_fft_tw, p->d_fft_post, p->d_four_a, p->d_four_b, p->d_proj};
+                    p->d_rowmu, p->d_fft_tw, p->d_fft_post, p->d_four_a, p->d_four_b, p->d_proj,
+                    p->d_xcoef, p->d_chk, p->d_chk_off};
     for (void* q : ptrs)
         if (q) cudaFree(q);
 }
@@ -156,7 +160,6 @@ static void plan_build(pswe_plan* p, int R, int nlat, int nlon, int mode) {
         nlon = dealiased_nlon(R);
         nlat = nlon / 2;
     }
-    if (nlat % 2) throw std::invalid_argument("pswe_plan_create: nlat must be even (latitude folding)");
     if (nlon % 2 || !five_smooth(nlon / 2))
         throw std::invalid_argument("pswe_plan_create: nlon must be even with nlon/2 5-smooth");
     if (nlon <= 2 * R) throw std::invalid_argument("pswe_plan_create: nlon must exceed 2R");
@@ -167,9 +170,10 @@ static void plan_build(pswe_plan* p, int R, int nlat, int nlon, int mode) {
     p->R = R;
     p->nlat = nlat;
     p->nlon = nlon;
-    p->J = nlat / 2;
+    p->J = (nlat + 1) / 2;  // latitude pairs (+ the equator row when nlat is odd)
     p->N = nlon / 2;
     p->legendre_mode = mode;
+    if (const char* e = std::getenv("PSWE_LEGENDRE_SIMT")) p->simt = std::atoi(e) != 0;
     p->K = num_coeffs(R);
     p->Kx = num_ext(R);
     const int J = p->J;
@@ -182,7 +186,7 @@ static void plan_build(pswe_plan* p, int R, int nlat, int nlon, int mode) {
 
     // north-half latitudes, seeds (legendre.cpp:26-29)
     std::vector<double> mu_n(J), seed((size_t)(R + 1) * J);
-    for (int j = 0; j < J; ++j) mu_n[j] = p->mu[nlat / 2 + j];
+    for (int j = 0; j < J; ++j) mu_n[j] = p->mu[nlat - J + j];
     for (int m = 0; m <= R; ++m) {
         const double la = sectoral_log_amplitude(m);
         for (int j = 0; j < J; ++j) {
@@ -250,6 +254,7 @@ static void plan_build(pswe_plan* p, int R, int nlat, int nlon, int mode) {
         build_ptab_kernel<<<grid, 128>>>(R, J, p->d_mu_n, p->d_seed, p->d_rec, p->d_ptab);
         PSWE_LAUNCH_CHECK();
     }
+    build_legendre_checkpoints(*p);
     p->reserve(1);
     PSWE_CUDA(cudaDeviceSynchronize());
 }

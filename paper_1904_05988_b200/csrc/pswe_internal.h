@@ -76,6 +76,7 @@ struct DevPlan;  // POD view of the plan passed to kernels
 struct pswe_plan {
     int R = 0, nlat = 0, nlon = 0, J = 0, N = 0;
     int legendre_mode = PSWE_LEGENDRE_RECOMPUTE;
+    int simt = 0;  // PSWE_LEGENDRE_SIMT=1 at plan creation: DFMA (CUDA-core) Legendre kernels
     int device = 0;
     long K = 0, Kx = 0;
     // host copies
@@ -86,6 +87,8 @@ struct pswe_plan {
     double2* d_rec = nullptr;    // [Kx] (1/eps(m,s+1), eps(m,s)/eps(m,s+1)) at off_ext(m)+s-m
     double* d_eps = nullptr;     // [Kx] eps(m, s) at off_ext(m)+s-m, s = m..R+1
     double* d_ptab = nullptr;    // STREAM mode: [Kx * J] P^m_s(mu_j), block m: [j][s]
+    double2* d_chk = nullptr;    // [sum_m ceil((R+2-m)/16)][J] (P_t, P_{t-1}) at t = 16c (forward DMMA)
+    int* d_chk_off = nullptr;    // [R+2] chunk offsets per m into d_chk
     double* d_rowc = nullptr;    // [nlat] cos(phi_i)
     double* d_roww = nullptr;    // [nlat] Gauss weight w_i
     double* d_rowmu = nullptr;   // [nlat] mu_i
@@ -97,6 +100,7 @@ struct pswe_plan {
     double2* d_four_a = nullptr;  // [cap * 5 * (R+1) * nlat] Fourier rows, [b][f][m][i]
     double2* d_four_b = nullptr;  // [cap * 5 * (R+1) * nlat]
     double2* d_proj = nullptr;    // [cap * 5 * Kx] Legendre projections, extended layout
+    double2* d_xcoef = nullptr;   // [cap * 5 * Kx] inverse-Legendre coefficients (U/V derived), ext layout
     void reserve(int batch);
 };
 
@@ -113,6 +117,12 @@ void legendre_inverse(const pswe_plan& P, int kind, const double2* in, const dou
 // projections; out_ext: extended layout [b][f][Kx] (s = m..R+1); else standard [b][f][K].
 void legendre_forward(const pswe_plan& P, const double2* four, int nf, int n_batch, double2* out,
                       bool out_ext, cudaStream_t st);
+// DMMA (FP64 tensor core) variants over nq complex columns (legendre_mma.cu)
+void legendre_inverse_mma(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq,
+                          double radius, double2* out, cudaStream_t st);
+void legendre_forward_mma(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
+                          cudaStream_t st);
+void build_legendre_checkpoints(pswe_plan& P);
 
 // fft.cu
 // Fourier rows [b][m][i] -> grid [b][i][j] (c2r, Im G_0 := 0), optional per-row 1/cos(phi).
