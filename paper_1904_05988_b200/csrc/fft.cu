@@ -143,8 +143,8 @@ __global__ void __launch_bounds__(256) fft_c2r_kernel(FftDesc fd, int R, int nla
     double2* buf = sm;
     double2* tmp = sm + N;
     const int i = blockIdx.x, b = blockIdx.y;
-    const double2* row = four + ((long)b * in_stride + in_off) * (R + 1) * nlat + i;
-    for (int k = threadIdx.x; k < N; k += blockDim.x) buf[k] = c2r_pre(row, nlat, k, N, R, post);
+    const double2* row = four + (((long)b * in_stride + in_off) * nlat + i) * (R + 1);
+    for (int k = threadIdx.x; k < N; k += blockDim.x) buf[k] = c2r_pre(row, 1, k, N, R, post);
     __syncthreads();
     fft_cplx<true>(buf, tmp, 1, fd, tw);
     const double c = div_cos ? 1.0 / rowc[i] : 1.0;
@@ -203,10 +203,10 @@ __global__ void __launch_bounds__(256) fft_eval_kernel(FftDesc fd, int R, int nl
     double2* tmp = sm + 5 * N;     // [G][N]
     const int i = blockIdx.x, b = blockIdx.y;
     const long rowsz = (long)(R + 1) * nlat;
-    const double2* in = four_in + (long)b * 4 * rowsz + i;
+    const double2* in = four_in + ((long)b * 4 * nlat + i) * (R + 1);
     for (int idx = threadIdx.x; idx < 4 * N; idx += blockDim.x) {
         const int f = idx / N, k = idx - f * N;
-        data[idx] = c2r_pre(in + f * rowsz, nlat, k, N, R, post);
+        data[idx] = c2r_pre(in + f * rowsz, 1, k, N, R, post);
     }
     __syncthreads();
     for (int f0 = 0; f0 < 4; f0 += G) fft_cplx<true>(data + (long)f0 * N, tmp, min(G, 4 - f0), fd, tw);
@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(256) fft_eval_kernel(FftDesc fd, int R, int nl
 void fft_rows_c2r(const pswe_plan& P, const double2* four, int in_stride, int in_off, double* grid, int n,
                   bool div_cos, cudaStream_t st) {
     if (n <= 0) return;
+    if (fft_rows_c2r_t(P, four, in_stride, in_off, grid, n, div_cos, st)) return;
     const size_t sm = 2 * (size_t)P.N * sizeof(double2);
     if (sm > 48 * 1024) PSWE_CUDA(cudaFuncSetAttribute(fft_c2r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     fft_c2r_kernel<<<dim3(P.nlat, n), 256, sm, st>>>(P.fft, P.R, P.nlat, P.d_fft_tw, P.d_fft_post, four, in_stride,
@@ -263,6 +264,7 @@ void fft_rows_c2r(const pswe_plan& P, const double2* four, int in_stride, int in
 void fft_rows_r2c(const pswe_plan& P, const double* grid, double2* four, int out_stride, int out_off, int n,
                   bool pre_cos, int scale_mode, double radius, cudaStream_t st) {
     if (n <= 0) return;
+    if (fft_rows_r2c_t(P, grid, four, out_stride, out_off, n, pre_cos, scale_mode, radius, st)) return;
     const size_t sm = 2 * (size_t)P.N * sizeof(double2);
     if (sm > 48 * 1024) PSWE_CUDA(cudaFuncSetAttribute(fft_r2c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     fft_r2c_kernel<<<dim3(P.nlat, n), 256, sm, st>>>(P.fft, P.R, P.nlat, P.d_fft_tw, P.d_fft_post, grid, four,
@@ -274,6 +276,7 @@ void fft_rows_r2c(const pswe_plan& P, const double* grid, double2* four, int out
 void fft_eval_products(const pswe_plan& P, const pswe_params& prm, const double2* four_in, double2* four_out,
                        int n_batch, cudaStream_t st) {
     if (n_batch <= 0) return;
+    if (fft_eval_products_t(P, prm, four_in, four_out, n_batch, st)) return;
     int G = 5;
     size_t sm = (size_t)(5 + G) * P.N * sizeof(double2);
     if (sm > 200 * 1024) {

@@ -147,9 +147,9 @@ __global__ void __launch_bounds__(64) leg_inv_kernel(int R, int J, int nlat, con
     const int iN = nlat - J + j, iS = J - 1 - j;  // iN == iS: equator (odd nlat)
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
-        double2* o = out + (((long)b * NF + f) * (R + 1) + m) * nlat;
-        o[iN] = make_double2(aE[f].x + aO[f].x, aE[f].y + aO[f].y);
-        o[iS] = make_double2(aE[f].x - aO[f].x, aE[f].y - aO[f].y);
+        double2* o = out + ((long)b * NF + f) * nlat * (R + 1) + m;  // rows [q][i][m]
+        o[(long)iN * (R + 1)] = make_double2(aE[f].x + aO[f].x, aE[f].y + aO[f].y);
+        o[(long)iS * (R + 1)] = make_double2(aE[f].x - aO[f].x, aE[f].y - aO[f].y);
     }
 }
 

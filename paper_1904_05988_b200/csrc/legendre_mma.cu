@@ -254,9 +254,10 @@ __global__ void __launch_bounds__(256) leg_inv_mma_kernel(int R, int J, int nlat
             if (q >= nq) continue;
             const double* e = acc[mt][0][nt];
             const double* o = acc[mt][1][nt];
-            double2* dst = out + ((long)q * (R + 1) + m) * nlat;
-            dst[iN] = make_double2(e[0] + o[0], e[1] + o[1]);
-            if (iS != iN) dst[iS] = make_double2(e[0] - o[0], e[1] - o[1]);
+            // latitude-major rows [q][i][m]: the FFT stage then reads contiguous rows
+            double2* dst = out + (long)q * nlat * (R + 1) + m;
+            dst[(long)iN * (R + 1)] = make_double2(e[0] + o[0], e[1] + o[1]);
+            if (iS != iN) dst[(long)iS * (R + 1)] = make_double2(e[0] - o[0], e[1] - o[1]);
         }
     }
 }

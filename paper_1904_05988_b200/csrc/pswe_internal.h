@@ -94,6 +94,7 @@ struct pswe_plan {
     double* d_rowmu = nullptr;   // [nlat] mu_i
     double2* d_fft_tw = nullptr; // stage twiddles
     double2* d_fft_post = nullptr;  // [N+1] exp(-2 pi i k / nlon)
+    double2* d_fft_roots = nullptr; // [N] exp(-2 pi i k / N) (compile-time-sized kernels, fft2.cu)
     pswe::FftDesc fft{};
     // scratch (grow-only)
     int cap_batch = 0;
@@ -138,6 +139,14 @@ void fft_rows_r2c(const pswe_plan& P, const double* grid, double2* four, int out
 // four_out [b][5][m][i] (Phi'U, Phi'V, qU, qV, ke), weights folded in.
 void fft_eval_products(const pswe_plan& P, const pswe_params& prm, const double2* four_in,
                        double2* four_out, int n_batch, cudaStream_t st);
+
+// fft2.cu: compile-time-sized variants; return false if nlon/2 is not instantiated
+bool fft_eval_products_t(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
+                         cudaStream_t st);
+bool fft_rows_c2r_t(const pswe_plan& P, const double2* four, int in_stride, int in_off, double* grid, int n,
+                    bool div_cos, cudaStream_t st);
+bool fft_rows_r2c_t(const pswe_plan& P, const double* grid, double2* four, int out_stride, int out_off, int n,
+                    bool pre_cos, int scale_mode, double radius, cudaStream_t st);
 
 // ops.cu
 void eval_tail(const pswe_plan& P, const pswe_params& prm, const double2* proj, const double2* state,
