@@ -55,6 +55,13 @@ typedef struct pswe_params {
 const char* pswe_last_error(void);
 int pswe_abi_version(void);
 
+/* ---- device memory / stream helpers for hosts without CUDA bindings (cgo, JNI, ctypes) */
+int pswe_device_alloc(unsigned long long bytes, void** out);
+int pswe_device_free(void* ptr);
+int pswe_memcpy_h2d(void* dst, const void* src, unsigned long long bytes, void* stream); /* async */
+int pswe_memcpy_d2h(void* dst, const void* src, unsigned long long bytes, void* stream); /* async */
+int pswe_stream_synchronize(void* stream);
+
 /* ---- host-side numerical setup (gauss.cpp:24-50, transform.cpp:38-43, quadrature.cpp:74-106) */
 int pswe_dealiased_nlon(int truncation);
 int pswe_gauss_latitudes(int n, double* mu, double* weight);

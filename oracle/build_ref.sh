@@ -19,3 +19,14 @@ g++ -std=c++20 -O3 -march=x86-64-v3 -fopenmp -fPIC -shared -include algorithm \
     -o "$OUT/libpintswe_ref.so.tmp" -lpthread
 mv "$OUT/libpintswe_ref.so.tmp" "$OUT/libpintswe_ref.so"
 echo "built $OUT/libpintswe_ref.so"
+
+# GpuImexOde drop-in: the reference's sdc/multilevel/pfasst sources + the adapter over libpswe.so
+PSWE_LIB_DIR="$(cd "$HERE/.." && pwd)/paper_1904_05988_b200"
+if [ -f "$PSWE_LIB_DIR/libpswe.so" ]; then
+  g++ -std=c++20 -O3 -march=x86-64-v3 -fopenmp -fPIC -shared -include algorithm \
+      -I"$REF/include" -I"$HERE/ref_build" -I"$HERE/../include" \
+      $FILES "$HERE/ref_build/gpu_imexode.cpp" -o "$OUT/libpintswe_gpu.so.tmp" \
+      -L"$PSWE_LIB_DIR" -lpswe -Wl,-rpath,'$ORIGIN/../../paper_1904_05988_b200' -lpthread
+  mv "$OUT/libpintswe_gpu.so.tmp" "$OUT/libpintswe_gpu.so"
+  echo "built $OUT/libpintswe_gpu.so"
+fi

@@ -29,6 +29,11 @@ class BlockConfig(ctypes.Structure):
 SIGNATURES = {
     "pswe_last_error": (ctypes.c_char_p, []),
     "pswe_abi_version": (_i, []),
+    "pswe_device_alloc": (_i, [ctypes.c_ulonglong, ctypes.POINTER(_vp)]),
+    "pswe_device_free": (_i, [_vp]),
+    "pswe_memcpy_h2d": (_i, [_vp, _vp, ctypes.c_ulonglong, _vp]),
+    "pswe_memcpy_d2h": (_i, [_vp, _vp, ctypes.c_ulonglong, _vp]),
+    "pswe_stream_synchronize": (_i, [_vp]),
     "pswe_dealiased_nlon": (_i, [_i]),
     "pswe_gauss_latitudes": (_i, [_i, _vp, _vp]),
     "pswe_quadrature_tables": (_i, [_i, _vp, _vp, _vp, _vp]),

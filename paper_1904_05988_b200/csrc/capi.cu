@@ -35,6 +35,25 @@ void eval_imex(pswe_plan& P, const pswe_params& prm, const double2* state, doubl
 
 extern "C" {
 
+int pswe_device_alloc(unsigned long long bytes, void** out) {
+    return guarded([&] {
+        need(out, "out");
+        PSWE_CUDA(cudaMalloc(out, bytes));
+    });
+}
+int pswe_device_free(void* ptr) {
+    return guarded([&] { PSWE_CUDA(cudaFree(ptr)); });
+}
+int pswe_memcpy_h2d(void* dst, const void* src, unsigned long long bytes, void* stream) {
+    return guarded([&] { PSWE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream))); });
+}
+int pswe_memcpy_d2h(void* dst, const void* src, unsigned long long bytes, void* stream) {
+    return guarded([&] { PSWE_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream))); });
+}
+int pswe_stream_synchronize(void* stream) {
+    return guarded([&] { PSWE_CUDA(cudaStreamSynchronize(as_stream(stream))); });
+}
+
 int pswe_synthesise(pswe_plan* P, const double* coeffs, double* grid, int n, void* stream) {
     return guarded([&] {
         need(P, "plan");
