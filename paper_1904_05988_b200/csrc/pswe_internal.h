@@ -94,7 +94,8 @@ struct pswe_plan {
     double* d_rowmu = nullptr;   // [nlat] mu_i
     double2* d_fft_tw = nullptr; // stage twiddles
     double2* d_fft_post = nullptr;  // [N+1] exp(-2 pi i k / nlon)
-    double2* d_fft_roots = nullptr; // [N] exp(-2 pi i k / N) (compile-time-sized kernels, fft2.cu)
+    double2* d_fft_roots = nullptr; // [N] exp(-2 pi i k / N)
+    double2* d_fft_ptw = nullptr;   // per-pass twiddles of the compile-time Stockham (fft2.cu)
     pswe::FftDesc fft{};
     // scratch (grow-only)
     int cap_batch = 0;
@@ -141,6 +142,7 @@ void fft_eval_products(const pswe_plan& P, const pswe_params& prm, const double2
                        double2* four_out, int n_batch, cudaStream_t st);
 
 // fft2.cu: compile-time-sized variants; return false if nlon/2 is not instantiated
+std::vector<double2> fft_pass_twiddles(int N);
 bool fft_eval_products_t(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
                          cudaStream_t st);
 bool fft_rows_c2r_t(const pswe_plan& P, const double2* four, int in_stride, int in_off, double* grid, int n,
