@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -208,6 +209,14 @@ struct pswe_pfasst {
     std::vector<cudaEvent_t> send_done[2];
     size_t send_next[2] = {0, 0};
     double* d_res_all = nullptr;
+    // serial emulation replays the whole block as one CUDA graph (captured on the 2nd call,
+    // after an eager call has sized every pool); theta0 is copied into d_theta first
+    bool use_graph = true;
+    int eager_runs = 0;
+    double2* d_theta = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
 };
 
 namespace {
@@ -359,6 +368,7 @@ int pswe_pfasst_create_serial(pswe_pair* pair, const pswe_block_config* cfg, psw
     return guarded([&] {
         if (!out) throw std::invalid_argument("out is NULL");
         auto* pf = new pswe_pfasst;
+        if (const char* e = std::getenv("PSWE_NO_GRAPH")) pf->use_graph = std::atoi(e) == 0;
         try {
             init_common(pf, pair, cfg);
         } catch (...) {
@@ -431,6 +441,11 @@ int pswe_pfasst_destroy(pswe_pfasst* pf) {
     return guarded([&] {
         if (!pf) return;
         cudaDeviceSynchronize();
+        if (pf->graph) cudaGraphExecDestroy(pf->graph);
+        if (pf->d_theta) cudaFree(pf->d_theta);
+        if (pf->gstream) cudaStreamDestroy(pf->gstream);
+        if (pf->ev_in) cudaEventDestroy(pf->ev_in);
+        if (pf->ev_out) cudaEventDestroy(pf->ev_out);
         cudaFree(pf->d_tau);
         cudaFree(pf->d_dstate0);
         cudaFree(pf->d_res);
@@ -463,7 +478,46 @@ int pswe_pfasst_run_block(pswe_pfasst* pf, const double* theta0, double* final_s
         const int n = pf->cfg.n_time_steps, N = pf->cfg.n_iter;
         PSWE_CUDA(cudaMemsetAsync(pf->d_res, 0, sizeof(double) * n * (N + 1), st));
         if (!pf->distributed) {
-            run_serial(pf, th, st);
+            if (!pf->use_graph) {
+                run_serial(pf, th, st);
+            } else {
+                // the block is a fixed sequence of ~10^2-10^3 small launches: capture it once and
+                // replay it (no host launch overhead, no host logic per kernel)
+                // capture/launch on an internal stream (the caller's may be the legacy default
+                // stream, which cannot be captured), ordered after / before the caller's stream
+                if (!pf->d_theta) {
+                    PSWE_CUDA(cudaMalloc(&pf->d_theta, state_bytes(pf->Kf)));
+                    PSWE_CUDA(cudaStreamCreateWithFlags(&pf->gstream, cudaStreamNonBlocking));
+                    PSWE_CUDA(cudaEventCreateWithFlags(&pf->ev_in, cudaEventDisableTiming));
+                    PSWE_CUDA(cudaEventCreateWithFlags(&pf->ev_out, cudaEventDisableTiming));
+                }
+                const cudaStream_t gs = pf->gstream;
+                PSWE_CUDA(cudaMemcpyAsync(pf->d_theta, th, state_bytes(pf->Kf), cudaMemcpyDeviceToDevice, st));
+                PSWE_CUDA(cudaEventRecord(pf->ev_in, st));
+                PSWE_CUDA(cudaStreamWaitEvent(gs, pf->ev_in, 0));
+                if (!pf->graph && pf->eager_runs >= 1) {
+                    cudaGraph_t g = nullptr;
+                    PSWE_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+                    try {
+                        run_serial(pf, pf->d_theta, gs);
+                    } catch (...) {
+                        cudaStreamEndCapture(gs, &g);
+                        if (g) cudaGraphDestroy(g);
+                        throw;
+                    }
+                    PSWE_CUDA(cudaStreamEndCapture(gs, &g));
+                    PSWE_CUDA(cudaGraphInstantiate(&pf->graph, g, 0));
+                    cudaGraphDestroy(g);
+                }
+                if (pf->graph) {
+                    PSWE_CUDA(cudaGraphLaunch(pf->graph, gs));
+                } else {
+                    run_serial(pf, pf->d_theta, gs);
+                    ++pf->eager_runs;
+                }
+                PSWE_CUDA(cudaEventRecord(pf->ev_out, gs));
+                PSWE_CUDA(cudaStreamWaitEvent(st, pf->ev_out, 0));
+            }
             if (final_state)
                 PSWE_CUDA(cudaMemcpyAsync(final_state, st_ptr(pf->fine, pf->mf - 1), state_bytes(pf->Kf),
                                           cudaMemcpyDeviceToDevice, st));
