@@ -373,7 +373,9 @@ void legendre_forward(const pswe_plan& P, const double2* four, int nf, int n_bat
                       cudaStream_t st) {
     if (n_batch <= 0) return;
     if (P.J > 1024) throw std::invalid_argument("legendre_forward: nlat > 2048 not supported");
-    if (P.legendre_mode == PSWE_LEGENDRE_STREAM) {
+    if (P.legendre_mode == PSWE_LEGENDRE_STREAM && !P.simt) {  // DMMA on the streamed table
+        legendre_forward_stream(P, four, nf * n_batch, out, ext, st);
+    } else if (P.legendre_mode == PSWE_LEGENDRE_STREAM) {
         if (nf % 5 == 0) fwd_stream<5>(P, four, nf, n_batch, out, ext, st);
         else if (nf % 2 == 0) fwd_stream<2>(P, four, nf, n_batch, out, ext, st);
         else fwd_stream<1>(P, four, nf, n_batch, out, ext, st);

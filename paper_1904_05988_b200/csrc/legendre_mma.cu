@@ -454,7 +454,8 @@ void legendre_inverse_mma(const pswe_plan& P, int kind, const double2* in, const
                           double2* out, cudaStream_t st) {
     if (nq <= 0) return;
     if (kind == INV_PLAIN) {
-        dispatch_inv<false>(P, in, nq, out, st);
+        if (P.legendre_mode == PSWE_LEGENDRE_STREAM && P.J <= 256) legendre_inverse_stream(P, false, in, nq, out, st);
+        else dispatch_inv<false>(P, in, nq, out, st);
         return;
     }
     const long Kx = P.Kx;
@@ -464,13 +465,19 @@ void legendre_inverse_mma(const pswe_plan& P, int kind, const double2* in, const
     if (kind == INV_EVAL) inv_prep_kernel<INV_EVAL><<<g, 128, 0, st>>>(P.R, P.d_eps, in, in2, radius, P.d_xcoef);
     else inv_prep_kernel<INV_UV><<<g, 128, 0, st>>>(P.R, P.d_eps, in, in2, radius, P.d_xcoef);
     PSWE_LAUNCH_CHECK();
-    dispatch_inv<true>(P, P.d_xcoef, nq, out, st);
+    // measured (tools/stage_times.py): the streamed inverse wins for J <= 256 latitude pairs, the
+    // recurrence inverse beyond (the table read is then larger than the recurrence's cost)
+    if (P.legendre_mode == PSWE_LEGENDRE_STREAM && P.J <= 256)
+        legendre_inverse_stream(P, true, P.d_xcoef, nq, out, st);
+    else
+        dispatch_inv<true>(P, P.d_xcoef, nq, out, st);
 }
 
 // Forward Legendre on DMMA over nq complex columns.
 void legendre_forward_mma(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
                           cudaStream_t st) {
     if (nq <= 0) return;
+    if (legendre_forward_mma2(P, four, nq, out, ext, st)) return;  // legendre_fwd2.cu (default)
     const int nsl = (P.J + 31) / 32;
     if (nq > 4 && nsl <= 16) launch_fwd<2>(P, four, nq, out, ext, st);
     else launch_fwd<1>(P, four, nq, out, ext, st);

@@ -141,7 +141,7 @@ void pswe_plan::reserve(int batch) {
 static void plan_free(pswe_plan* p) {
     void* ptrs[] = {p->d_mu_n, p->d_seed, p->d_rec, p->d_eps, p->d_ptab, p->d_rowc, p->d_roww,
                     p->d_rowmu, p->d_fft_tw, p->d_fft_post, p->d_four_a, p->d_four_b, p->d_proj,
-                    p->d_xcoef, p->d_chk, p->d_chk_off, p->d_fft_roots, p->d_fft_ptw};
+                    p->d_xcoef, p->d_chk, p->d_chk_off, p->d_fft_roots, p->d_fft_ptw, p->d_ptab2};
     for (void* q : ptrs)
         if (q) cudaFree(q);
 }
@@ -255,13 +255,14 @@ static void plan_build(pswe_plan* p, int R, int nlat, int nlon, int mode) {
     p->d_fft_roots = upload(roots);
     p->d_fft_ptw = upload(fft_pass_twiddles(p->N));
 
-    if (mode == PSWE_LEGENDRE_STREAM) {
+    if (mode == PSWE_LEGENDRE_STREAM && p->simt) {  // table of the DFMA (SIMT) stream kernel
         PSWE_CUDA(cudaMalloc(&p->d_ptab, (size_t)p->Kx * J * sizeof(double)));
         dim3 grid((J + 127) / 128, R + 1);
         build_ptab_kernel<<<grid, 128>>>(R, J, p->d_mu_n, p->d_seed, p->d_rec, p->d_ptab);
         PSWE_LAUNCH_CHECK();
     }
     build_legendre_checkpoints(*p);
+    if (mode == PSWE_LEGENDRE_STREAM) build_legendre_table2(*p);
     p->reserve(1);
     PSWE_CUDA(cudaDeviceSynchronize());
 }

@@ -89,6 +89,7 @@ struct pswe_plan {
     double* d_ptab = nullptr;    // STREAM mode: [Kx * J] P^m_s(mu_j), block m: [j][s]
     double2* d_chk = nullptr;    // [sum_m ceil((R+2-m)/16)][J] (P_t, P_{t-1}) at t = 16c (forward DMMA)
     int* d_chk_off = nullptr;    // [R+2] chunk offsets per m into d_chk
+    double* d_ptab2 = nullptr;   // STREAM mode: P tiles [m][chunk][Jp][par][8] (legendre_stream.cu)
     double* d_rowc = nullptr;    // [nlat] cos(phi_i)
     double* d_roww = nullptr;    // [nlat] Gauss weight w_i
     double* d_rowmu = nullptr;   // [nlat] mu_i
@@ -125,6 +126,14 @@ void legendre_inverse_mma(const pswe_plan& P, int kind, const double2* in, const
 void legendre_forward_mma(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
                           cudaStream_t st);
 void build_legendre_checkpoints(pswe_plan& P);
+bool legendre_forward_mma2(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
+                           cudaStream_t st);
+// STREAM mode (legendre_stream.cu): DMMA contractions on a streamed P table
+void build_legendre_table2(pswe_plan& P);
+void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
+                             cudaStream_t st);
+void legendre_inverse_stream(const pswe_plan& P, bool ext_layout, const double2* X, int nq, double2* out,
+                             cudaStream_t st);
 
 // fft.cu
 // Fourier rows [b][m][i] -> grid [b][i][j] (c2r, Im G_0 := 0), optional per-row 1/cos(phi).

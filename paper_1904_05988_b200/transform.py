@@ -51,7 +51,7 @@ class TransformPlan:
     dealiased grid; an explicit Gaussian grid may be given (BASELINE's linear grids)."""
 
     def __init__(self, truncation: int, nlat: int = 0, nlon: int = 0,
-                 legendre_mode: int = LEGENDRE_RECOMPUTE):
+                 legendre_mode: int = LEGENDRE_STREAM):
         if not torch.cuda.is_available():
             raise _lib.PsweError("TransformPlan needs a CUDA device (libpswe has no CPU path)")
         torch.cuda.init()
