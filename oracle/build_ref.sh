@@ -14,8 +14,12 @@ mkdir -p "$OUT"
 SRCS="gauss legendre transform reference swe quadrature sdc multilevel pfasst analysis"
 FILES=""
 for s in $SRCS; do FILES="$FILES $REF/src/$s.cpp"; done
+# io.cpp needs nlohmann/json (vendor/ is absent, proj/.gitignore:2); use the copy in the image if any
+JSON_DIR=/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+IOFLAGS=""
+if [ -f "$JSON_DIR/json.hpp" ]; then IOFLAGS="-I$JSON_DIR -DPSWE_REF_WITH_IO"; FILES="$FILES $REF/src/io.cpp"; fi
 g++ -std=c++20 -O3 -march=x86-64-v3 -fopenmp -fPIC -shared -include algorithm \
-    -I"$REF/include" -I"$HERE/ref_build" $FILES "$HERE/ref_build/ref_capi.cpp" \
+    -I"$REF/include" -I"$HERE/ref_build" $IOFLAGS $FILES "$HERE/ref_build/ref_capi.cpp" \
     -o "$OUT/libpintswe_ref.so.tmp" -lpthread
 mv "$OUT/libpintswe_ref.so.tmp" "$OUT/libpintswe_ref.so"
 echo "built $OUT/libpintswe_ref.so"
@@ -24,7 +28,7 @@ echo "built $OUT/libpintswe_ref.so"
 PSWE_LIB_DIR="$(cd "$HERE/.." && pwd)/paper_1904_05988_b200"
 if [ -f "$PSWE_LIB_DIR/libpswe.so" ]; then
   g++ -std=c++20 -O3 -march=x86-64-v3 -fopenmp -fPIC -shared -include algorithm \
-      -I"$REF/include" -I"$HERE/ref_build" -I"$HERE/../include" \
+      -I"$REF/include" -I"$HERE/ref_build" -I"$HERE/../include" $IOFLAGS \
       $FILES "$HERE/ref_build/gpu_imexode.cpp" -o "$OUT/libpintswe_gpu.so.tmp" \
       -L"$PSWE_LIB_DIR" -lpswe -Wl,-rpath,'$ORIGIN/../../paper_1904_05988_b200' -lpthread
   mv "$OUT/libpintswe_gpu.so.tmp" "$OUT/libpintswe_gpu.so"

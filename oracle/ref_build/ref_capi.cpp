@@ -459,3 +459,20 @@ int ref_mlsdc_run(int Rf, int nlat_f, int nlon_f, int Rc, int nlat_c, int nlon_c
 double ref_last_wall() { return g_last_wall; }
 
 }  // extern "C"
+
+// ---- io.cpp (JSON checkpoints, io.cpp:48-67): compiled only when nlohmann/json is available
+#ifdef PSWE_REF_WITH_IO
+#include "pintswe/io.hpp"
+extern "C" {
+int ref_save_checkpoint(const char* path, int R, const double* state, double time) {
+    return guard([&] { io::save_checkpoint(path, state_in(R, state), time); });
+}
+int ref_load_checkpoint(const char* path, int R, double* state, double* time) {
+    return guard([&] {
+        const PrognosticState s = io::load_checkpoint(path, time);
+        if (s.truncation() != R) throw std::invalid_argument("checkpoint truncation mismatch");
+        state_out(s, state);
+    });
+}
+}
+#endif

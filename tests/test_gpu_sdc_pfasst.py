@@ -111,3 +111,20 @@ def test_pfasst_serial_emulation(P, golden, n_ts, n_blocks, mode):
     ref_log = sorted(tuple(int(v) for v in m) for m in golden[f"pf_nts{n_ts}_msgs"])
     mine = sorted((m[0], m[1], ord(m[2]), m[3], m[4], m[5], m[6]) for m in pf.messages())
     assert mine == ref_log
+
+
+def test_pfasst_nccl_executor_single_rank(P, golden):
+    """The NCCL executor on one GPU (world = 1): communicator set-up, the final-state broadcast and
+    the residual all-gather; the result must equal the serial-emulation / reference run."""
+    pytest.importorskip("torch")
+    pair, _ = _pair(P)
+    try:
+        uid = P.pfasst.nccl_unique_id()
+    except Exception as e:  # NCCL not loadable on this machine
+        pytest.skip(f"NCCL unavailable: {e}")
+    pf = P.Pfasst(pair, P.BlockConfig(1, 60.0, 3), rank=0, world=1, nccl_id=uid)
+    fin, hist = P.run_blocks(pf, cuda(golden["pf_theta0"]), 1)
+    fin = host(fin)
+    assert rel_diff_fields(fin, golden["pf_nts1_final"]) < 1e-10
+    assert res_ok(hist, golden["pf_nts1_res"], fin)
+    pf.close()
