@@ -12,6 +12,7 @@
 // inverse  E/O[j][col]  = sum_t P[j][t] X[t][col]:         A = P tile, B = X (smem)
 // P tile in smem: [32 latitudes][20] (8 even, 8 odd, 4 pad): both fragment patterns hit two
 // conflict-free wavefronts (row stride = 4 mod 16 doubles).
+#include <cmath>
 #include <cstdlib>
 
 #include "pswe_internal.h"
@@ -310,16 +311,28 @@ void inv_launch(const pswe_plan& P, const double2* X, int nq, double2* out, cuda
 
 template <bool EXT>
 void inv_dispatch(const pswe_plan& P, const double2* X, int nq, double2* out, cudaStream_t st) {
-    int best = 1, best_cost = 1 << 30;
-    for (int nt = 4; nt >= 1; --nt) {
-        const int groups = (nq + 4 * nt - 1) / (4 * nt);
-        const int cost = groups * nt * 8 + groups;  // padded n-tiles first, then table re-reads
-        if (cost < best_cost) {
-            best_cost = cost;
-            best = nt;
+    // cost per (chunk, slice) in shared-memory wavefronts + DMMA issue: a block of NT n-tiles
+    // issues 16 NT DMMA (x16 cycles) against 16 P-fragment + 4 NT X-fragment loads (2 wavefronts
+    // each, shared by the SM's 4 SMSPs), plus one P tile (32 wavefronts) per column group.
+    // Measured (tools/stage_times.py): NT = 5 (one group of 20 columns: 0.45 fragment loads per
+    // DMMA, 252 registers) wins for a 5-state batch once there are >= 192 latitude pairs to fill
+    // the machine; otherwise the fewest padded n-tiles, then the fewest groups.
+    int best = 1;
+    if (nq >= 20 && nq % 20 == 0 && P.J >= 192) {
+        best = 5;
+    } else {
+        int best_cost = 1 << 30;
+        for (int nt = 4; nt >= 1; --nt) {
+            const int groups = (nq + 4 * nt - 1) / (4 * nt);
+            const int cost = groups * nt * 8 + groups;
+            if (cost < best_cost) {
+                best_cost = cost;
+                best = nt;
+            }
         }
     }
     switch (best) {
+        case 5: inv_launch<EXT, 5>(P, X, nq, out, st); break;
         case 4: inv_launch<EXT, 4>(P, X, nq, out, st); break;
         case 3: inv_launch<EXT, 3>(P, X, nq, out, st); break;
         case 2: inv_launch<EXT, 2>(P, X, nq, out, st); break;
