@@ -477,7 +477,6 @@ void legendre_inverse_mma(const pswe_plan& P, int kind, const double2* in, const
 void legendre_forward_mma(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
                           cudaStream_t st) {
     if (nq <= 0) return;
-    if (legendre_forward_mma2(P, four, nq, out, ext, st)) return;  // legendre_fwd2.cu (default)
     const int nsl = (P.J + 31) / 32;
     if (nq > 4 && nsl <= 16) launch_fwd<2>(P, four, nq, out, ext, st);
     else launch_fwd<1>(P, four, nq, out, ext, st);

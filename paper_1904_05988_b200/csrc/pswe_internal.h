@@ -126,8 +126,6 @@ void legendre_inverse_mma(const pswe_plan& P, int kind, const double2* in, const
 void legendre_forward_mma(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
                           cudaStream_t st);
 void build_legendre_checkpoints(pswe_plan& P);
-bool legendre_forward_mma2(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
-                           cudaStream_t st);
 // STREAM mode (legendre_stream.cu): DMMA contractions on a streamed P table
 void build_legendre_table2(pswe_plan& P);
 void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
