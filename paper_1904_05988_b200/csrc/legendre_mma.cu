@@ -19,7 +19,7 @@
 // Fragment layouts (CuTe SM80_8x4 / SM80_8x8_Row): A[m = lane>>2][k = lane&3],
 // B[k = lane&3][n = lane>>2], C[m = lane>>2][n = 2(lane&3) + v]. Tile strides make every
 // fragment load two conflict-free shared-memory wavefronts.
-#include "pswe_internal.h"
+#include "legendre_common.cuh"
 
 namespace pswe {
 
@@ -296,23 +296,8 @@ __global__ void __launch_bounds__(256) leg_fwd_mma_kernel(int R, int J, int nlat
     const long Kx = (long)(R + 1) * (R + 4) / 2, K = (long)(R + 1) * (R + 2) / 2;
 
     // stage G_E = G_N + G_S and G_O = G_N - G_S (Gauss weights folded in by the FFT stage)
-    for (int idx = threadIdx.x; idx < Jp * 4 * NT; idx += blockDim.x) {
-        const int ql = idx / Jp, jj = idx - ql * Jp;  // latitude fastest: coalesced rows
-        const int q = q0 + ql;
-        double2 e = make_double2(0.0, 0.0), o = e;
-        if (jj < J && q < nq) {
-            const double2* src = four + ((long)q * (R + 1) + m) * nlat;
-            const int iN = nlat - J + jj, iS = J - 1 - jj;
-            const double2 gn = src[iN];
-            const double2 gs = (iN == iS) ? make_double2(0.0, 0.0) : src[iS];
-            e = make_double2(gn.x + gs.x, gn.y + gs.y);
-            o = make_double2(gn.x - gs.x, gn.y - gs.y);
-        }
-        G[jj * SG + 2 * ql] = e.x;
-        G[jj * SG + 2 * ql + 1] = e.y;
-        G[(Jp + jj) * SG + 2 * ql] = o.x;
-        G[(Jp + jj) * SG + 2 * ql + 1] = o.y;
-    }
+    legc::stage_g<NT, 8>(G, Jp * SG, Jp, J, nlat, R, m, q0, nq, four,
+                         [](int j, int col) { return j * SG + col; });
     for (int jj = threadIdx.x; jj < Jp; jj += blockDim.x) mus[jj] = jj < J ? mu_n[jj] : 0.0;
     for (int t = threadIdx.x; t < len; t += blockDim.x) rcs[t] = rec[bx + t];
     __syncthreads();

@@ -15,7 +15,7 @@
 #include <cmath>
 #include <cstdlib>
 
-#include "pswe_internal.h"
+#include "legendre_common.cuh"
 
 namespace pswe {
 
@@ -112,25 +112,16 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
     const long Kx = (long)(R + 1) * (R + 4) / 2, K = (long)(R + 1) * (R + 2) / 2;
     const double* __restrict__ pm = ptab + (long)cbase[m] * Jp * 16;
 
-    for (int idx = threadIdx.x; idx < Jp * 4 * NT; idx += blockDim.x) {
-        const int ql = idx / Jp, jj = idx - ql * Jp;
-        const int q = q0 + ql;
-        double2 e = make_double2(0.0, 0.0), o = e;
-        if (jj < J && q < nq) {
-            const double2* src = four + ((long)q * (R + 1) + m) * nlat;
-            const int iN = nlat - J + jj, iS = J - 1 - jj;
-            const double2 gn = src[iN];
-            const double2 gs = (iN == iS) ? make_double2(0.0, 0.0) : src[iS];
-            e = make_double2(gn.x + gs.x, gn.y + gs.y);
-            o = make_double2(gn.x - gs.x, gn.y - gs.y);
-        }
-        G[gpos<NT>(jj, 2 * ql)] = e.x;
-        G[gpos<NT>(jj, 2 * ql + 1)] = e.y;
-        G[Jp * SG + gpos<NT>(jj, 2 * ql)] = o.x;
-        G[Jp * SG + gpos<NT>(jj, 2 * ql + 1)] = o.y;
+    // first P tile of this warp's first chunk streams in while G is staged
+    if (warp < nch) {
+        load_tile(tiles, pm + (long)warp * Jp * 16, lane);
+        cp_async_commit();
     }
+    legc::stage_g<NT, 8>(G, Jp * SG, Jp, J, nlat, R, m, q0, nq, four,
+                         [](int j, int col) { return gpos<NT>(j, col); });
     __syncthreads();
     const int r4 = lane >> 2, c4 = lane & 3;
+    bool first = true;
 
     for (int c = warp; c < nch; c += W) {
         double acc[2][NT][2];  // [par][nt]: C[col 8nt + r4][deg-in-parity 2 c4 + v]
@@ -139,8 +130,11 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
 #pragma unroll
             for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
         const double* src = pm + (long)c * Jp * 16;
-        load_tile(tiles, src, lane);
-        cp_async_commit();
+        if (!first) {  // the first task's tile was issued before the G staging
+            load_tile(tiles, src, lane);
+            cp_async_commit();
+        }
+        first = false;
         for (int sl = 0; sl < nsl; ++sl) {
             if (sl + 1 < nsl) load_tile(tiles + ((sl + 1) & 1) * 32 * ST, src + (long)(sl + 1) * 32 * 16, lane);
             cp_async_commit();
@@ -212,14 +206,13 @@ __global__ void __launch_bounds__(256) leg_inv_stream_mma_kernel(int R, int J, i
     const int r4 = lane >> 2, c4 = lane & 3;
 
     // X chunk: 16 degrees x NQ complex columns -> xs[tl][2 ql + v], zero beyond tlim / nq
+    // asynchronous (cp.async, zero-filled) so it overlaps the DMMAs of the previous chunk
     auto stage_x = [&](double* dst, int t0) {
         for (int idx = lane; idx < CH * NQ; idx += 32) {
             const int ql = idx / CH, tl = idx - ql * CH;  // degree fastest
             const int t = t0 + tl, q = q0 + ql;
-            double2 v = make_double2(0.0, 0.0);
-            if (t < tlim && q < nq) v = X[(long)q * Kq + base + t];
-            dst[tl * SX + 2 * ql] = v.x;
-            dst[tl * SX + 2 * ql + 1] = v.y;
+            const bool v = t < tlim && q < nq;
+            legc::cp_async16z(dst + tl * SX + 2 * ql, v ? (const void*)(X + (long)q * Kq + base + t) : (const void*)X, v);
         }
     };
 
@@ -232,11 +225,14 @@ __global__ void __launch_bounds__(256) leg_inv_stream_mma_kernel(int R, int J, i
             for (int cc = 0; cc < NT; ++cc) acc[a][b][cc][0] = acc[a][b][cc][1] = 0.0;
 
     load_tile(tiles, pm, lane);
-    cp_async_commit();
     stage_x(xs, 0);
+    cp_async_commit();
     for (int c = 0; c < nch; ++c) {
         const int b = c & 1;
-        if (c + 1 < nch) load_tile(tiles + (b ^ 1) * 32 * ST, pm + (long)(c + 1) * Jp * 16, lane);
+        if (c + 1 < nch) {
+            load_tile(tiles + (b ^ 1) * 32 * ST, pm + (long)(c + 1) * Jp * 16, lane);
+            stage_x(xs + (b ^ 1) * CH * SX, (c + 1) * CH);
+        }
         cp_async_commit();
         cp_async_wait<1>();
         __syncwarp();
@@ -258,7 +254,6 @@ __global__ void __launch_bounds__(256) leg_inv_stream_mma_kernel(int R, int J, i
                     for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][par][nt], af[mt], bf[nt]);
             }
         }
-        if (c + 1 < nch) stage_x(xs + (b ^ 1) * CH * SX, (c + 1) * CH);
         __syncwarp();
     }
     cp_async_wait<0>();
@@ -283,7 +278,11 @@ __global__ void __launch_bounds__(256) leg_inv_stream_mma_kernel(int R, int J, i
 
 template <int NT>
 void fwd_launch(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext, cudaStream_t st) {
-    const int W = 8;
+    // warps per block: the block stages G for every latitude (smem ~ Jp), so small J wants
+    // small blocks (more blocks per SM, staging overlapped across blocks) and large J wants
+    // more warps sharing one staged tile. PSWE_FWD_WARPS overrides (tuning only).
+    static const int w_env = [] { const char* e = getenv("PSWE_FWD_WARPS"); return e ? atoi(e) : 0; }();
+    const int W = w_env > 0 ? w_env : (P.J <= 256 ? 4 : 8);
     const int Jp = ((P.J + 31) / 32) * 32;
     const int groups = (nq + 4 * NT - 1) / (4 * NT);
     const size_t sm = (size_t)(2 * Jp * 8 * NT + W * 2 * 32 * ST) * sizeof(double);
