@@ -276,6 +276,7 @@ void fft_rows_r2c(const pswe_plan& P, const double* grid, double2* four, int out
 void fft_eval_products(const pswe_plan& P, const pswe_params& prm, const double2* four_in, double2* four_out,
                        int n_batch, cudaStream_t st) {
     if (n_batch <= 0) return;
+    if (fft_eval_products_ip(P, prm, four_in, four_out, n_batch, st)) return;
     if (fft_eval_products_t(P, prm, four_in, four_out, n_batch, st)) return;
     int G = 5;
     size_t sm = (size_t)(5 + G) * P.N * sizeof(double2);

@@ -1,0 +1,284 @@
+// In-place longitude FFT stage of eval_nonlinear (sm_100a, fp64).
+//
+// Replaces the ping-pong Stockham kernel of fft2.cu for the fused grid stage (swe.cpp:41-54 with
+// the FFT halves of uv_from_vortdiv / synthesise / vortdiv_from_uv / analyse, transform.cpp:
+// 101-190). One block per (latitude row, state) holds the 5 complex rows of length N = nlon/2 in
+// shared memory ONCE (no scratch copy):
+//
+//   load + c2r pre-pass   X_k (k <= R) of Phi, zeta, U, V -> Z_k, natural order (pair k, N-k
+//                         owned by one thread, straight from global memory)
+//   inverse DIF passes    in place; the grid leaves in mixed-radix digit-reversed order
+//   grid-point products   pointwise, so the permuted order does not matter (4 -> 5 rows)
+//   forward DIT passes    in place, the exact transpose of the DIF: digit-reversed in, natural out
+//   r2c post-pass         X_k = 1/2 (Z_k + conj Z_{N-k}) - i/2 W^k (Z_k - conj Z_{N-k}), k <= R,
+//                         Gauss weight / cos^2 scaling folded, rows [q][m][i] to global
+//
+// Radix plans end with a radix-8 pass and the shared layout pads one slot per 8 (ipad), which
+// makes every pass's 16-byte accesses conflict-free for j-fastest thread mapping (checked with a
+// bank model for all instantiated N). Half the shared memory of the ping-pong form, no copy-back
+// passes and no separate pre-pass phase: 8 barriers per block instead of 12.
+#include <cmath>
+#include <cstdlib>
+
+#include "fft_t.cuh"
+
+namespace pswe {
+
+using namespace fftt;
+
+namespace {
+
+constexpr int kIpThreads = 256;
+
+// radix of pass s (0 = first) of the in-place plan for length N; 0 past the last pass.
+// Plans: head(N/8) then a final radix-8 pass.
+__host__ __device__ constexpr int ip_radix(int N, int s) {
+    const int h = N / 8;
+    int h0 = 0, h1 = 0;
+    switch (h) {
+        case 3: h0 = 3; break;
+        case 4: h0 = 4; break;
+        case 6: h0 = 6; break;
+        case 8: h0 = 8; break;
+        case 12: h0 = 12; break;
+        case 16: h0 = 16; break;
+        case 24: h0 = 8; h1 = 3; break;
+        case 32: h0 = 4; h1 = 8; break;
+        case 48: h0 = 8; h1 = 6; break;
+        case 64: h0 = 8; h1 = 8; break;
+        case 96: h0 = 12; h1 = 8; break;
+        case 128: h0 = 16; h1 = 8; break;
+        case 192: h0 = 12; h1 = 16; break;
+        default: return 0;
+    }
+    if (s == 0) return h0;
+    if (h1) return s == 1 ? h1 : (s == 2 ? 8 : 0);
+    return s == 1 ? 8 : 0;
+}
+__host__ __device__ constexpr int ip_npass(int N) {
+    int s = 0;
+    while (ip_radix(N, s)) ++s;
+    return s;
+}
+__host__ __device__ constexpr int ip_len(int N, int s) {  // sub-transform length entering pass s
+    int n = N;
+    for (int r = 0; r < s; ++r) n /= ip_radix(N, r);
+    return n;
+}
+__host__ __device__ constexpr int ip_off(int N, int s) {  // twiddle table offset of pass s
+    int o = 0;
+    for (int r = 0; r < s; ++r) o += (ip_radix(N, r) - 1) * (ip_len(N, r) / ip_radix(N, r));
+    return o;
+}
+
+__device__ __forceinline__ int ipad(int i) { return i + (i >> 3); }
+__host__ __device__ constexpr int ipadded(int n) { return n + (n >> 3); }
+
+// DIF pass s on G rows of A: sub-blocks of length n, butterflies over t (stride M), then the
+// twiddle w_n^(j k) on output k; outputs back to the same slots.
+template <int N, int s, int G, bool INV>
+__device__ __forceinline__ void dif_pass(double2* A, const double2* __restrict__ TW) {
+    constexpr int P = ip_radix(N, s), n = ip_len(N, s), M = n / P, OFF = ip_off(N, s);
+    constexpr int T = G * N / P;
+    for (int it = threadIdx.x; it < T; it += kIpThreads) {
+        const int j = it % M;
+        const int base = (it - j) * P + j;  // (it / M) n + j
+        double2 v[P];
+#pragma unroll
+        for (int t = 0; t < P; ++t) v[t] = A[ipad(base + t * M)];
+        double2 w[P > 1 ? P - 1 : 1];
+        if constexpr (M > 1) {
+#pragma unroll
+            for (int k = 1; k < P; ++k) w[k - 1] = __ldg(TW + OFF + (k - 1) * M + j);
+        }
+        dft<P, INV>(v);
+        A[ipad(base)] = v[0];
+#pragma unroll
+        for (int k = 1; k < P; ++k) {
+            double2 o = v[k];
+            if constexpr (M > 1) o = cmul(o, INV ? cconj(w[k - 1]) : w[k - 1]);
+            A[ipad(base + k * M)] = o;
+        }
+    }
+}
+
+// DIT pass s (transpose of dif_pass): twiddle w_n^(j t) on input t, then the butterfly.
+template <int N, int s, int G, bool INV>
+__device__ __forceinline__ void dit_pass(double2* A, const double2* __restrict__ TW) {
+    constexpr int P = ip_radix(N, s), n = ip_len(N, s), M = n / P, OFF = ip_off(N, s);
+    constexpr int T = G * N / P;
+    for (int it = threadIdx.x; it < T; it += kIpThreads) {
+        const int j = it % M;
+        const int base = (it - j) * P + j;
+        double2 v[P];
+#pragma unroll
+        for (int t = 0; t < P; ++t) v[t] = A[ipad(base + t * M)];
+        if constexpr (M > 1) {
+#pragma unroll
+            for (int t = 1; t < P; ++t) {
+                const double2 w = __ldg(TW + OFF + (t - 1) * M + j);
+                v[t] = cmul(v[t], INV ? cconj(w) : w);
+            }
+        }
+        dft<P, INV>(v);
+#pragma unroll
+        for (int k = 0; k < P; ++k) A[ipad(base + k * M)] = v[k];
+    }
+}
+
+template <int N, int s, int G, bool INV>
+struct DifGuard {
+    __device__ static void run(double2* A, const double2* TW) {
+        if constexpr (s < ip_npass(N)) {
+            dif_pass<N, s, G, INV>(A, TW);
+            __syncthreads();
+            DifGuard<N, s + 1, G, INV>::run(A, TW);
+        }
+    }
+};
+template <int N, int s, int G, bool INV>
+struct DitGuard {  // passes s, s-1, ..., 0
+    __device__ static void run(double2* A, const double2* TW) {
+        if constexpr (s >= 0) {
+            dit_pass<N, s, G, INV>(A, TW);
+            __syncthreads();
+            DitGuard<N, s - 1, G, INV>::run(A, TW);
+        }
+    }
+};
+
+// Z_k of the half-length c2r trick from X_k and X_{N-k} (fft2.cu c2r_pre_s)
+__device__ __forceinline__ double2 c2r_z(double2 a, double2 bb, double2 w) {
+    const double2 b = cconj(bb);
+    const double2 e = cadd(a, b);
+    const double2 o = cmul(csub(a, b), cconj(w));
+    return make_double2(e.x - o.y, e.y + o.x);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kIpThreads, (N <= 512 ? 3 : 1))
+    fft_eval_ip_kernel(int R, int nlat, const double2* __restrict__ TW, const double2* __restrict__ post,
+                       const double2* __restrict__ four_in, double2* __restrict__ four_out,
+                       const double* __restrict__ rowc, const double* __restrict__ roww,
+                       const double* __restrict__ rowmu, double phi_bar, double omega, double inv_a) {
+    extern __shared__ double2 A[];  // [5][N], ipad layout
+    const int i = blockIdx.x, b = blockIdx.y;
+    const long rowsz = (long)(R + 1) * nlat;
+    const double2* in = four_in + ((long)b * 4 * nlat + i) * (R + 1);  // rows [q][i][m]
+
+    // load + pre-pass: task (f, k), k = 0..N/2, owns Z_k and Z_{N-k}; all loads issued first
+    constexpr int H = N / 2 + 1;
+    constexpr int U = (4 * H + kIpThreads - 1) / kIpThreads;
+    double2 xa[U], xb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int it = threadIdx.x + u * kIpThreads;
+        xa[u] = xb[u] = make_double2(0.0, 0.0);
+        if (it < 4 * H) {
+            const int f = it / H, k = it - f * H;
+            if (k <= R) xa[u] = in[f * rowsz + k];
+            if (k > 0 && N - k <= R) xb[u] = in[f * rowsz + N - k];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int it = threadIdx.x + u * kIpThreads;
+        if (it < 4 * H) {
+            const int f = it / H, k = it - f * H;
+            double2 a = xa[u];
+            if (k == 0) a.y = 0.0;  // Im G_0 := 0
+            A[ipad(f * N + k)] = c2r_z(a, xb[u], __ldg(post + k));
+            if (k > 0 && k < N / 2) A[ipad(f * N + N - k)] = c2r_z(xb[u], xa[u], __ldg(post + N - k));
+        }
+    }
+    __syncthreads();
+    DifGuard<N, 0, 4, true>::run(A, TW);
+
+    // grid-point products (swe.cpp:41-54), two grid points per complex slot, slot order permuted
+    const double c = rowc[i];
+    const double ic = 1.0 / c;
+    const double fc = 2.0 * omega * rowmu[i];
+    for (int k = threadIdx.x; k < N; k += kIpThreads) {
+        const int p = ipad(k);
+        constexpr int RS = ipadded(N);
+        const double2 ph = A[p], ze = A[RS + p], U2 = A[2 * RS + p], V2 = A[3 * RS + p];
+        double o[5][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double Uh = h ? U2.y : U2.x, Vh = h ? V2.y : V2.x;
+            const double uu = Uh * ic, vv = Vh * ic;
+            const double phip = (h ? ph.y : ph.x) - phi_bar;
+            const double absv = (h ? ze.y : ze.x) + fc;
+            o[0][h] = (phip * uu) * c;
+            o[1][h] = (phip * vv) * c;
+            o[2][h] = (absv * uu) * c;
+            o[3][h] = (absv * vv) * c;
+            o[4][h] = 0.5 * (uu * uu + vv * vv);
+        }
+#pragma unroll
+        for (int q = 0; q < 5; ++q) A[q * RS + p] = make_double2(o[q][0], o[q][1]);
+    }
+    __syncthreads();
+    DitGuard<N, ip_npass(N) - 1, 5, false>::run(A, TW);
+
+    const double nl = 2.0 * N;
+    const double sflux = (1.0 / nl) * (inv_a * roww[i] / (c * c));
+    const double ske = (1.0 / nl) * roww[i];
+    double2* out = four_out + (long)b * 5 * rowsz + i;
+    for (int it = threadIdx.x; it < 5 * (R + 1); it += kIpThreads) {
+        const int q = it / (R + 1), k = it - q * (R + 1);
+        const double2 zk = A[ipad(q * N + k)];
+        const double2 zc = cconj(A[ipad(q * N + (k == 0 ? 0 : N - k))]);
+        const double2 e = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
+        const double2 d = csub(zk, zc);
+        const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);
+        const double2 x = cadd(e, cmul(__ldg(post + k), o));
+        const double sc = q < 4 ? sflux : ske;
+        out[q * rowsz + (long)k * nlat] = make_double2(x.x * sc, x.y * sc);
+    }
+}
+
+template <int N>
+bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n, cudaStream_t st) {
+    const size_t sm = (size_t)5 * ipadded(N) * sizeof(double2);
+    auto kern = fft_eval_ip_kernel<N>;
+    if (sm > 48 * 1024) PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kern<<<dim3(P.nlat, n), kIpThreads, sm, st>>>(P.R, P.nlat, P.d_fft_iptw, P.d_fft_post, fin, fout, P.d_rowc,
+                                                  P.d_roww, P.d_rowmu, prm.phi_bar, prm.omega, 1.0 / prm.radius);
+    PSWE_LAUNCH_CHECK();
+    return true;
+}
+
+}  // namespace
+
+// Twiddles of the in-place plan: pass s (P, M, n = P M): entries OFF_s + (k-1) M + j =
+// exp(-2 pi i j k / n), k = 1..P-1, j = 0..M-1. Empty (one dummy entry) if N has no plan.
+std::vector<double2> fft_ip_twiddles(int N) {
+    std::vector<double2> tw;
+    for (int s = 0; ip_radix(N, s); ++s) {
+        const int P = ip_radix(N, s), n = ip_len(N, s), M = n / P;
+        for (int k = 1; k < P; ++k)
+            for (int j = 0; j < M; ++j) {
+                const long double a = -2.0L * 3.141592653589793238462643383279502884L * ((long)j * k % n) / n;
+                tw.push_back(make_double2((double)std::cos(a), (double)std::sin(a)));
+            }
+    }
+    if (tw.empty()) tw.push_back(make_double2(1.0, 0.0));
+    return tw;
+}
+
+bool fft_eval_products_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
+                          cudaStream_t st) {
+    static const bool off = [] { const char* e = getenv("PSWE_FFT_STOCKHAM"); return e && atoi(e) != 0; }();
+    if (off) return false;
+    switch (P.N) {
+#define PSWE_CASE(NN) \
+    case NN: return eval_ip<NN>(P, prm, fin, fout, n, st);
+        PSWE_CASE(24) PSWE_CASE(32) PSWE_CASE(48) PSWE_CASE(64) PSWE_CASE(96) PSWE_CASE(128) PSWE_CASE(192)
+        PSWE_CASE(256) PSWE_CASE(384) PSWE_CASE(512) PSWE_CASE(768) PSWE_CASE(1024) PSWE_CASE(1536)
+#undef PSWE_CASE
+        default: return false;
+    }
+}
+
+}  // namespace pswe

@@ -57,6 +57,30 @@ __device__ __forceinline__ double2 w16(double2 a) {
     return make_double2(a.x * c - a.y * s, a.x * s + a.y * c);
 }
 
+// multiply by w_12^k = exp(-+2 pi i k / 12) (compile-time k)
+__device__ constexpr double kC12[12] = {1.0,
+                                        0.86602540378443864676,
+                                        0.5,
+                                        0.0,
+                                        -0.5,
+                                        -0.86602540378443864676,
+                                        -1.0,
+                                        -0.86602540378443864676,
+                                        -0.5,
+                                        0.0,
+                                        0.5,
+                                        0.86602540378443864676};
+template <int K, bool INV>
+__device__ __forceinline__ double2 w12(double2 a) {
+    constexpr int k = K % 12;
+    if constexpr (k == 0) return a;
+    if constexpr (k == 3) return rot<INV>(a);
+    if constexpr (k == 6) return make_double2(-a.x, -a.y);
+    if constexpr (k == 9) return rot<!INV>(a);
+    const double c = kC12[k], s = INV ? kC12[(k + 9) % 12] : -kC12[(k + 9) % 12];  // sin = cos(k - 3)
+    return make_double2(a.x * c - a.y * s, a.x * s + a.y * c);
+}
+
 template <bool INV>
 __device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2, double2& x3) {
     const double2 b0 = cadd(x0, x2), b1 = csub(x0, x2), b2 = cadd(x1, x3);
@@ -99,6 +123,43 @@ __device__ __forceinline__ void dft(double2 (&x)[P]) {
         x[4] = csub(e1, f1);
         x[2] = cadd(e2, f2);
         x[3] = csub(e2, f2);
+    } else if constexpr (P == 6) {
+        // 3 x 2: a = DFT3(x0, x2, x4), b = DFT3(x1, x3, x5) w6^k; y_k = a_k + b_k, y_{k+3} = a_k - b_k
+        double2 a[3] = {x[0], x[2], x[4]}, b[3] = {x[1], x[3], x[5]};
+        dft<3, INV>(a);
+        dft<3, INV>(b);
+        b[1] = w12<2, INV>(b[1]);
+        b[2] = w12<4, INV>(b[2]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            x[k] = cadd(a[k], b[k]);
+            x[k + 3] = csub(a[k], b[k]);
+        }
+    } else if constexpr (P == 12) {
+        // 3 x 4: n = n2 + 4 n1; A[n2] = DFT3 over n1, twiddle w12^(n2 k1), DFT4 over n2 -> k1 + 3 k2
+        double2 f[4][3];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            f[r][0] = x[r];
+            f[r][1] = x[r + 4];
+            f[r][2] = x[r + 8];
+            dft<3, INV>(f[r]);
+        }
+        f[1][1] = w12<1, INV>(f[1][1]);
+        f[1][2] = w12<2, INV>(f[1][2]);
+        f[2][1] = w12<2, INV>(f[2][1]);
+        f[2][2] = w12<4, INV>(f[2][2]);
+        f[3][1] = w12<3, INV>(f[3][1]);
+        f[3][2] = w12<6, INV>(f[3][2]);
+#pragma unroll
+        for (int k1 = 0; k1 < 3; ++k1) {
+            double2 a = f[0][k1], b = f[1][k1], c = f[2][k1], d = f[3][k1];
+            dft4<INV>(a, b, c, d);
+            x[k1] = a;
+            x[k1 + 3] = b;
+            x[k1 + 6] = c;
+            x[k1 + 9] = d;
+        }
     } else if constexpr (P == 8) {
         // DIT 2 x 4: E = DFT4(even), O = DFT4(odd); y_k = E_k + w8^k O_k, y_{k+4} = E_k - w8^k O_k
         double2 e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6];

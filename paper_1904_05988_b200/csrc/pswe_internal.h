@@ -97,6 +97,7 @@ struct pswe_plan {
     double2* d_fft_post = nullptr;  // [N+1] exp(-2 pi i k / nlon)
     double2* d_fft_roots = nullptr; // [N] exp(-2 pi i k / N)
     double2* d_fft_ptw = nullptr;   // per-pass twiddles of the compile-time Stockham (fft2.cu)
+    double2* d_fft_iptw = nullptr;  // per-pass twiddles of the in-place DIF/DIT plan (fft_ip.cu)
     pswe::FftDesc fft{};
     // scratch (grow-only)
     int cap_batch = 0;
@@ -150,6 +151,10 @@ void fft_eval_products(const pswe_plan& P, const pswe_params& prm, const double2
 
 // fft2.cu: compile-time-sized variants; return false if nlon/2 is not instantiated
 std::vector<double2> fft_pass_twiddles(int N);
+// fft_ip.cu: in-place fused grid stage; false if nlon/2 has no in-place plan
+std::vector<double2> fft_ip_twiddles(int N);
+bool fft_eval_products_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
+                          cudaStream_t st);
 bool fft_eval_products_t(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
                          cudaStream_t st);
 bool fft_rows_c2r_t(const pswe_plan& P, const double2* four, int in_stride, int in_off, double* grid, int n,

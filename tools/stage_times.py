@@ -1,5 +1,6 @@
 """Per-kernel device times of one eval_imex call (CUDA events between the launches) for a few
-truncations and batch sizes. Usage: python tools/stage_times.py"""
+truncations and batch sizes. Usage: python tools/stage_times.py [R:nlat:nlon ...] (nlat 0 = default
+grid); with sizes given only those run, at batch 5."""
 import ctypes
 import os
 import sys
@@ -16,9 +17,14 @@ from paper_1904_05988_b200.transform import _stream  # noqa: E402
 L = _lib.lib()
 prm = P.ModelParams(phi_bar=9.80616e4)
 cp = prm.c()
-for R, nlat, nlon in ((63, 0, 0), (127, 0, 0), (255, 0, 0), (255, 256, 512), (511, 0, 0), (1023, 1024, 2048)):
+SIZES = ((63, 0, 0), (127, 0, 0), (255, 0, 0), (255, 256, 512), (511, 0, 0), (1023, 1024, 2048))
+BATCHES = (1, 5)
+if len(sys.argv) > 1:
+    SIZES = [tuple(int(x) for x in a.split(':')) for a in sys.argv[1:]]
+    BATCHES = (5,)
+for R, nlat, nlon in SIZES:
     plan = P.TransformPlan(R, nlat, nlon, int(os.environ.get('LEGENDRE_MODE', '0')))
-    for n in (1, 5):
+    for n in BATCHES:
         plan.reserve(n)
         st = torch.as_tensor(np.stack([balanced_random_state(R, 40.0, 7 + i) for i in range(n)])).cuda()
         fi, fe = torch.empty_like(st), torch.empty_like(st)
