@@ -30,6 +30,7 @@ namespace {
 
 constexpr int kIpThreads = 256;
 
+
 // radix of pass s (0 = first) of the in-place plan for length N; 0 past the last pass.
 // Plans: head(N/8) then a final radix-8 pass.
 __host__ __device__ constexpr int ip_radix(int N, int s) {
@@ -71,13 +72,24 @@ __host__ __device__ constexpr int ip_off(int N, int s) {  // twiddle table offse
     return o;
 }
 
+// blocks per SM the register budget is sized for: 4 (64 registers) when every radix is <= 8,
+// fewer for the radix-12/16 plans (their butterflies alone hold 24-32 doubles)
+__host__ __device__ constexpr int ip_minblocks(int N) {
+    int mx = 0;
+    for (int s = 0; ip_radix(N, s); ++s) mx = ip_radix(N, s) > mx ? ip_radix(N, s) : mx;
+    if (mx <= 8) return N <= 512 ? 4 : 2;
+    return N <= 768 ? 2 : 1;
+}
+
+__host__ __device__ constexpr int ip_ntw(int N) { return ip_off(N, ip_npass(N)); }  // twiddle entries
+
 __device__ __forceinline__ int ipad(int i) { return i + (i >> 3); }
 __host__ __device__ constexpr int ipadded(int n) { return n + (n >> 3); }
 
 // DIF pass s on G rows of A: sub-blocks of length n, butterflies over t (stride M), then the
 // twiddle w_n^(j k) on output k; outputs back to the same slots.
 template <int N, int s, int G, bool INV>
-__device__ __forceinline__ void dif_pass(double2* A, const double2* __restrict__ TW) {
+__device__ __forceinline__ void dif_pass(double2* A, const double2* TW) {
     constexpr int P = ip_radix(N, s), n = ip_len(N, s), M = n / P, OFF = ip_off(N, s);
     constexpr int T = G * N / P;
     for (int it = threadIdx.x; it < T; it += kIpThreads) {
@@ -89,7 +101,7 @@ __device__ __forceinline__ void dif_pass(double2* A, const double2* __restrict__
         double2 w[P > 1 ? P - 1 : 1];
         if constexpr (M > 1) {
 #pragma unroll
-            for (int k = 1; k < P; ++k) w[k - 1] = __ldg(TW + OFF + (k - 1) * M + j);
+            for (int k = 1; k < P; ++k) w[k - 1] = TW[OFF + (k - 1) * M + j];
         }
         dft<P, INV>(v);
         A[ipad(base)] = v[0];
@@ -104,7 +116,7 @@ __device__ __forceinline__ void dif_pass(double2* A, const double2* __restrict__
 
 // DIT pass s (transpose of dif_pass): twiddle w_n^(j t) on input t, then the butterfly.
 template <int N, int s, int G, bool INV>
-__device__ __forceinline__ void dit_pass(double2* A, const double2* __restrict__ TW) {
+__device__ __forceinline__ void dit_pass(double2* A, const double2* TW) {
     constexpr int P = ip_radix(N, s), n = ip_len(N, s), M = n / P, OFF = ip_off(N, s);
     constexpr int T = G * N / P;
     for (int it = threadIdx.x; it < T; it += kIpThreads) {
@@ -116,7 +128,7 @@ __device__ __forceinline__ void dit_pass(double2* A, const double2* __restrict__
         if constexpr (M > 1) {
 #pragma unroll
             for (int t = 1; t < P; ++t) {
-                const double2 w = __ldg(TW + OFF + (t - 1) * M + j);
+                const double2 w = TW[OFF + (t - 1) * M + j];
                 v[t] = cmul(v[t], INV ? cconj(w) : w);
             }
         }
@@ -156,13 +168,21 @@ __device__ __forceinline__ double2 c2r_z(double2 a, double2 bb, double2 w) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(kIpThreads, (N <= 512 ? 3 : 1))
+__global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
     fft_eval_ip_kernel(int R, int nlat, const double2* __restrict__ TW, const double2* __restrict__ post,
                        const double2* __restrict__ four_in, double2* __restrict__ four_out,
                        const double* __restrict__ rowc, const double* __restrict__ roww,
                        const double* __restrict__ rowmu, double phi_bar, double omega, double inv_a) {
-    extern __shared__ double2 A[];  // [5][N], ipad layout
+    extern __shared__ double2 A[];  // [5][N], ipad layout; then the twiddles [ip_ntw(N)]
+    double2* sTW = A + 5 * ipadded(N);
     const int i = blockIdx.x, b = blockIdx.y;
+    // twiddles to shared memory (cp.async, overlapped with the row loads; waited before the
+    // first barrier)
+    for (int t = threadIdx.x; t < ip_ntw(N); t += kIpThreads) {
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sTW + t));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(TW + t));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
     const long rowsz = (long)(R + 1) * nlat;
     const double2* in = four_in + ((long)b * 4 * nlat + i) * (R + 1);  // rows [q][i][m]
 
@@ -191,8 +211,9 @@ __global__ void __launch_bounds__(kIpThreads, (N <= 512 ? 3 : 1))
             if (k > 0 && k < N / 2) A[ipad(f * N + N - k)] = c2r_z(xb[u], xa[u], __ldg(post + N - k));
         }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
-    DifGuard<N, 0, 4, true>::run(A, TW);
+    DifGuard<N, 0, 4, true>::run(A, sTW);
 
     // grid-point products (swe.cpp:41-54), two grid points per complex slot, slot order permuted
     const double c = rowc[i];
@@ -219,30 +240,41 @@ __global__ void __launch_bounds__(kIpThreads, (N <= 512 ? 3 : 1))
         for (int q = 0; q < 5; ++q) A[q * RS + p] = make_double2(o[q][0], o[q][1]);
     }
     __syncthreads();
-    DitGuard<N, ip_npass(N) - 1, 5, false>::run(A, TW);
+    DitGuard<N, ip_npass(N) - 1, 5, false>::run(A, sTW);
 
     const double nl = 2.0 * N;
     const double sflux = (1.0 / nl) * (inv_a * roww[i] / (c * c));
     const double ske = (1.0 / nl) * roww[i];
     double2* out = four_out + (long)b * 5 * rowsz + i;
-    for (int it = threadIdx.x; it < 5 * (R + 1); it += kIpThreads) {
-        const int q = it / (R + 1), k = it - q * (R + 1);
-        const double2 zk = A[ipad(q * N + k)];
-        const double2 zc = cconj(A[ipad(q * N + (k == 0 ? 0 : N - k))]);
-        const double2 e = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
-        const double2 d = csub(zk, zc);
-        const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);
-        const double2 x = cadd(e, cmul(__ldg(post + k), o));
-        const double sc = q < 4 ? sflux : ske;
-        out[q * rowsz + (long)k * nlat] = make_double2(x.x * sc, x.y * sc);
+    for (int k = threadIdx.x; k <= R; k += kIpThreads) {
+        const double2 w = __ldg(post + k);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const double2 zk = A[ipad(q * N + k)];
+            const double2 zc = cconj(A[ipad(q * N + (k == 0 ? 0 : N - k))]);
+            const double2 e = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
+            const double2 d = csub(zk, zc);
+            const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);
+            const double2 x = cadd(e, cmul(w, o));
+            const double sc = q < 4 ? sflux : ske;
+            out[q * rowsz + (long)k * nlat] = make_double2(x.x * sc, x.y * sc);
+        }
     }
 }
 
 template <int N>
 bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n, cudaStream_t st) {
-    const size_t sm = (size_t)5 * ipadded(N) * sizeof(double2);
+    const size_t sm = (size_t)(5 * ipadded(N) + ip_ntw(N)) * sizeof(double2);
     auto kern = fft_eval_ip_kernel<N>;
-    if (sm > 48 * 1024) PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    static bool attr = false;  // once per instantiation
+    if (!attr) {
+        if (sm > 48 * 1024)
+            PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        // several blocks per SM only fit with the whole unified L1 given to shared memory
+        PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
+        attr = true;
+    }
     kern<<<dim3(P.nlat, n), kIpThreads, sm, st>>>(P.R, P.nlat, P.d_fft_iptw, P.d_fft_post, fin, fout, P.d_rowc,
                                                   P.d_roww, P.d_rowmu, prm.phi_bar, prm.omega, 1.0 / prm.radius);
     PSWE_LAUNCH_CHECK();
