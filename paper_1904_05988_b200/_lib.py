@@ -9,7 +9,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpswe.so")
+# PSWE_LIB_VARIANT=x loads libpswe_x.so from the same directory (A/B builds of tuning macros)
+LIB_PATH = os.path.join(_HERE, "libpswe.so" if not os.environ.get("PSWE_LIB_VARIANT")
+                        else f"libpswe_{os.environ['PSWE_LIB_VARIANT']}.so")
 
 _i, _d, _vp = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
 _pi = ctypes.POINTER(ctypes.c_int)

@@ -78,7 +78,7 @@ __host__ __device__ constexpr int ip_minblocks(int N) {
     int mx = 0;
     for (int s = 0; ip_radix(N, s); ++s) mx = ip_radix(N, s) > mx ? ip_radix(N, s) : mx;
     if (mx <= 8) return N <= 512 ? 4 : 2;
-    return N <= 768 ? 2 : 1;
+    return N <= 1024 ? 2 : 1;
 }
 
 __host__ __device__ constexpr int ip_ntw(int N) { return ip_off(N, ip_npass(N)); }  // twiddle entries
