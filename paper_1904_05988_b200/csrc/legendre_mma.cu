@@ -28,48 +28,9 @@ namespace {
 constexpr int CH = 16;  // degrees per chunk
 constexpr int XC = 64;  // inverse: degrees per staged coefficient super-chunk
 
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-        : "+d"(d[0]), "+d"(d[1])
-        : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ double2 inv_lap_at(const double2* __restrict__ x, long bs, int m, int R, int t, double a2) {
-    if (t < m || t > R || t == 0) return make_double2(0.0, 0.0);
-    const double f = -a2 / (t * (t + 1.0));
-    const double2 v = x[bs + t - m];
-    return make_double2(v.x * f, v.y * f);
-}
-
-__device__ __forceinline__ double2 hcoef(const double2* __restrict__ x, const double* __restrict__ eps, long bs,
-                                         long bx, int m, int R, int t, double a2) {
-    double2 c = make_double2(0.0, 0.0);
-    if (t - 1 >= m) {
-        const double2 pm = inv_lap_at(x, bs, m, R, t - 1, a2);
-        const double f = -(double)(t - 1) * eps[bx + t - m];
-        c.x += f * pm.x;
-        c.y += f * pm.y;
-    }
-    if (t + 1 <= R) {
-        const double2 pp = inv_lap_at(x, bs, m, R, t + 1, a2);
-        const double f = (double)(t + 2) * eps[bx + t + 1 - m];
-        c.x += f * pp.x;
-        c.y += f * pp.y;
-    }
-    return c;
-}
-
-// (r, s) of r-major index k
-__device__ __forceinline__ void decode_rs(int R, long k, int& m, int& s) {
-    const double b = 2.0 * R + 3.0;
-    int mm = (int)floor((b - sqrt(b * b - 8.0 * (double)k)) * 0.5);
-    if (mm < 0) mm = 0;
-    if (mm > R) mm = R;
-    while (mm > 0 && off_std(R, mm) > k) --mm;
-    while (mm < R && off_std(R, mm + 1) <= k) ++mm;
-    m = mm;
-    s = mm + (int)(k - off_std(R, mm));
-}
+using legc::dmma;
+using legc::hcoef;
+using legc::inv_lap_at;
 
 // (m, t) of extended index kx (t = s - m, s = m..R+1)
 __device__ __forceinline__ void decode_ext(int R, long kx, int& m, int& t) {
@@ -439,8 +400,16 @@ void legendre_inverse_mma(const pswe_plan& P, int kind, const double2* in, const
                           double2* out, cudaStream_t st) {
     if (nq <= 0) return;
     if (kind == INV_PLAIN) {
-        if (P.legendre_mode == PSWE_LEGENDRE_STREAM && P.J <= 256) legendre_inverse_stream(P, false, in, nq, out, st);
-        else dispatch_inv<false>(P, in, nq, out, st);
+        if (P.legendre_mode == PSWE_LEGENDRE_STREAM && P.J <= 256)
+            legendre_inverse_stream(P, kind, in, in2, nq, radius, out, st);
+        else
+            dispatch_inv<false>(P, in, nq, out, st);
+        return;
+    }
+    // measured (tools/stage_times.py): the streamed inverse wins for J <= 256 latitude pairs, the
+    // recurrence inverse beyond (the table read is then larger than the recurrence's cost)
+    if (P.legendre_mode == PSWE_LEGENDRE_STREAM && P.J <= 256) {
+        legendre_inverse_stream(P, kind, in, in2, nq, radius, out, st);
         return;
     }
     const long Kx = P.Kx;
@@ -450,12 +419,7 @@ void legendre_inverse_mma(const pswe_plan& P, int kind, const double2* in, const
     if (kind == INV_EVAL) inv_prep_kernel<INV_EVAL><<<g, 128, 0, st>>>(P.R, P.d_eps, in, in2, radius, P.d_xcoef);
     else inv_prep_kernel<INV_UV><<<g, 128, 0, st>>>(P.R, P.d_eps, in, in2, radius, P.d_xcoef);
     PSWE_LAUNCH_CHECK();
-    // measured (tools/stage_times.py): the streamed inverse wins for J <= 256 latitude pairs, the
-    // recurrence inverse beyond (the table read is then larger than the recurrence's cost)
-    if (P.legendre_mode == PSWE_LEGENDRE_STREAM && P.J <= 256)
-        legendre_inverse_stream(P, true, P.d_xcoef, nq, out, st);
-    else
-        dispatch_inv<true>(P, P.d_xcoef, nq, out, st);
+    dispatch_inv<true>(P, P.d_xcoef, nq, out, st);
 }
 
 // Forward Legendre on DMMA over nq complex columns.

@@ -4,14 +4,18 @@
 // and the checkpoint loads from the contraction kernels.
 //
 // Table layout (built once per plan by the same recurrence, legendre.cpp:30-37):
-//   ptab[(cbase(m) + c) * J * 16 + j * 16 + par * 8 + i] = P^m_{m + 16c + par + 2i}(mu_j)
-// i.e. per m, per 16-degree chunk c, per latitude j: the 8 even then the 8 odd degrees. A
-// (chunk, 32-latitude slice) tile is one contiguous 4 KB block. Degrees past R+1 are zero.
+//   ptab[(cbase(m) + c) * Jp * 16 + j * 16 + (col ^ ((j & 3) << 2))] = P^m_{m + 16c + tl}(mu_j),
+//   col = (tl & 1) * 8 + (tl >> 1)
+// i.e. per m, per 16-degree chunk c, per latitude j: the 8 even then the 8 odd degrees, XOR-
+// swizzled within the row. A (chunk, 32-latitude slice) tile is one contiguous 4 KB block that is
+// exactly its shared-memory image: one bulk copy, and both fragment patterns below read it in two
+// conflict-free wavefronts. Degrees past R+1 are zero.
 //
 // forward  Y^T[col][t] = sum_j G_par^T[col][j] P[j][t]:  A = G^T (smem, swizzled), B = P tile
-// inverse  E/O[j][col]  = sum_t P[j][t] X[t][col]:         A = P tile, B = X (smem)
-// P tile in smem: [32 latitudes][20] (8 even, 8 odd, 4 pad): both fragment patterns hit two
-// conflict-free wavefronts (row stride = 4 mod 16 doubles).
+// inverse  E/O[j][col]  = sum_t P[j][t] X[t][col]:         A = P tile, B = X tile (smem)
+// The inverse's X operand is written by its prep kernel directly as per-chunk shared-memory
+// images ([16 degrees][8 NT + 2] doubles), so each pipeline stage is W + 1 bulk copies (TMA,
+// cp.async.bulk) completing on one mbarrier; stages are released through a second mbarrier.
 #include <cmath>
 #include <cstdlib>
 
@@ -22,13 +26,11 @@ namespace pswe {
 namespace {
 
 constexpr int CH = 16;
-constexpr int ST = 20;  // smem P-tile row stride (doubles)
 
-__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-        : "+d"(d[0]), "+d"(d[1])
-        : "d"(a), "d"(b));
-}
+using legc::dmma;
+
+// swizzled column of degree-slot col (0..15) in latitude row j of a P tile
+__host__ __device__ __forceinline__ int pswz(int j, int col) { return col ^ ((j & 3) << 2); }
 
 __device__ __forceinline__ double rec_step(double2 ab, double mu, double p, double pm1) {
     return __fma_rn(ab.x, __dmul_rn(mu, p), -__dmul_rn(ab.y, pm1));
@@ -42,14 +44,47 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// copy one (chunk, slice) tile: 32 rows x 128 B -> smem [32][ST]; 8 x 16 B per lane
+// copy one (chunk, slice) tile (4 KB, already its smem image); 8 x 16 B per lane
 __device__ __forceinline__ void load_tile(double* dst, const double* __restrict__ src, int lane) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
         const int idx = u * 32 + lane;  // 256 16-byte pieces
-        const int row = idx >> 3, piece = idx & 7;
-        cp_async16(dst + row * ST + 2 * piece, src + row * 16 + 2 * piece);
+        cp_async16(dst + 2 * idx, src + 2 * idx);
     }
+}
+
+// ---- mbarrier + bulk-copy (TMA) primitives ---------------------------------------------------
+__device__ __forceinline__ unsigned sm_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sm_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(sm_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            sm_addr(dst)),
+        "l"(src), "r"(bytes), "r"(sm_addr(bar))
+        : "memory");
 }
 
 // table builder: thread per (m, j)
@@ -72,7 +107,7 @@ __global__ void build_ptab2_kernel(int R, int J, int Jp, const double* __restric
     double p = seed[(long)m * J + j], pm1 = 0.0;
     for (int t = 0; t < nch * CH; ++t) {
         const int c = t / CH, tl = t % CH;
-        out[(long)c * Jp * 16 + (tl & 1) * 8 + (tl >> 1)] = t < len ? p : 0.0;
+        out[(long)c * Jp * 16 + pswz(j, (tl & 1) * 8 + (tl >> 1))] = t < len ? p : 0.0;
         if (t < len) {
             const double pn = rec_step(__ldg(rc + t), mu, p, pm1);
             pm1 = p;
@@ -105,7 +140,7 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
     const int len = R + 2 - m;
     const int nch = (len + CH - 1) / CH;
     double* G = smem;                                       // [2][Jp][SG] swizzled
-    double* tiles = smem + 2 * Jp * SG + warp * (2 * 32 * ST);  // [2][32][ST] per warp
+    double* tiles = smem + 2 * Jp * SG + warp * (2 * 32 * 16);  // [2][32][16] per warp
     const int q0 = blockIdx.y * 4 * NT;
     const int tmax = ext ? len : len - 1;
     const long bx = off_ext(R, m);
@@ -136,17 +171,17 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
         }
         first = false;
         for (int sl = 0; sl < nsl; ++sl) {
-            if (sl + 1 < nsl) load_tile(tiles + ((sl + 1) & 1) * 32 * ST, src + (long)(sl + 1) * 32 * 16, lane);
+            if (sl + 1 < nsl) load_tile(tiles + ((sl + 1) & 1) * 32 * 16, src + (long)(sl + 1) * 32 * 16, lane);
             cp_async_commit();
             cp_async_wait<1>();
             __syncwarp();
-            const double* tl = tiles + (sl & 1) * 32 * ST;
+            const double* tl = tiles + (sl & 1) * 32 * 16;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
                 const int jk = sl * 32 + 4 * ks + c4;  // latitude of this lane's k
 #pragma unroll
                 for (int par = 0; par < 2; ++par) {
-                    const double bf = tl[(4 * ks + c4) * ST + par * 8 + r4];  // B[k=lat][n=degree]
+                    const double bf = tl[(4 * ks + c4) * 16 + pswz(c4, par * 8 + r4)];  // B[k=lat][n=degree]
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) {
                         const double af = G[par * Jp * SG + gpos<NT>(jk, 8 * nt + r4)];  // A[m=col][k=lat]
@@ -178,43 +213,112 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
 }
 
 // ---- inverse ------------------------------------------------------------------------------
-// grid (ceil(nslices / W), R+1, column groups); warp = 32-latitude slice walking all chunks;
-// X (prep output / input fields) staged per chunk by each warp; P tiles by cp.async.
-template <bool EXT, int NT>
-__global__ void __launch_bounds__(256) leg_inv_stream_mma_kernel(int R, int J, int Jp, int nlat, int nq,
-                                                                 const double* __restrict__ ptab,
-                                                                 const int* __restrict__ cbase,
-                                                                 const double2* __restrict__ X,
-                                                                 double2* __restrict__ out) {
-    constexpr int SX = 8 * NT + 2;  // X tile stride (2 SX = 4 mod 16)
-    constexpr int NQ = 4 * NT;
-    extern __shared__ double smem[];
-    const int W = blockDim.x >> 5;
+// X tiles: per column group z (4 NT complex columns from q0 = 4 NT z), per chunk (cbase(m) + c):
+// [16 degrees tl][8 NT + 2] doubles, column 2 ql + {re, im}, two zero pad columns; degree
+// t = 16 c + tl of order m (extended t = 0..R+1-m; standard t = 0..R-m), zero beyond.
+// prep: thread (tl, ql) of block (chunk, z) computes one complex entry (transform.cpp:204-206
+// with the H-sums as P-sums): EVAL q = 4 state + {Phi, zeta, U, V}, UV q = 2 pair + {U, V},
+// PLAIN q = field (standard layout, copied).
+template <int KIND>
+__global__ void xtile_prep_kernel(int R, int NQ, int SX, int nq, int nct, const int* __restrict__ chunk_m,
+                                  const int* __restrict__ cbase, const double* __restrict__ eps,
+                                  const double2* __restrict__ in, const double2* __restrict__ in2, double radius,
+                                  double* __restrict__ Xt) {
+    const int cg = blockIdx.x, z = blockIdx.y;
+    const int ql = threadIdx.x % NQ, tl = threadIdx.x / NQ;
+    const int m = chunk_m[cg];
+    const int t = (cg - cbase[m]) * CH + tl;
+    const int s = m + t;
+    const int q = z * NQ + ql;
+    const long K = (long)(R + 1) * (R + 2) / 2;
+    const long bs = off_std(R, m), bx = off_ext(R, m);
+    double2 v = make_double2(0.0, 0.0);
+    if (q < nq) {
+        if (KIND == INV_PLAIN) {
+            if (s <= R) v = in[(long)q * K + bs + t];
+        } else if (s <= R + 1) {
+            const double a2 = radius * radius, inv_a = 1.0 / radius;
+            int f;
+            const double2 *vort, *div;
+            if (KIND == INV_EVAL) {
+                const int b = q >> 2;
+                f = q & 3;
+                const double2* st = in + (long)b * 3 * K;
+                vort = st + K;
+                div = st + 2 * K;
+                if (f < 2) {
+                    if (s <= R) v = (f == 0 ? st : vort)[bs + t];
+                    f = -1;
+                }
+            } else {
+                const int pr = q >> 1;
+                f = 2 + (q & 1);
+                vort = in + (long)pr * K;
+                div = in2 + (long)pr * K;
+            }
+            if (f == 2) {
+                const double2 chi = legc::inv_lap_at(div, bs, m, R, s, a2);
+                const double2 cpsi = legc::hcoef(vort, eps, bs, bx, m, R, s, a2);
+                v = make_double2(inv_a * (-m * chi.y - cpsi.x), inv_a * (m * chi.x - cpsi.y));
+            } else if (f == 3) {
+                const double2 psi = legc::inv_lap_at(vort, bs, m, R, s, a2);
+                const double2 cchi = legc::hcoef(div, eps, bs, bx, m, R, s, a2);
+                v = make_double2(inv_a * (-m * psi.y + cchi.x), inv_a * (m * psi.x + cchi.y));
+            }
+        }
+    }
+    double* row = Xt + ((long)z * nct + cg) * CH * SX + (long)tl * SX;
+    *reinterpret_cast<double2*>(row + 2 * ql) = v;
+    if (ql == 0) *reinterpret_cast<double2*>(row + 2 * NQ) = make_double2(0.0, 0.0);
+}
+
+// grid (ceil(nslices / W), R+1, column groups); warp = 32-latitude slice walking all chunks of
+// its m; an S-stage ring of {W P tiles, one X tile} per block, filled by bulk copies issued by
+// thread 0 (full[s]: expect_tx + complete_tx) and released by one arrival per warp (empty[s]).
+template <int NT, int W, int S>
+__global__ void __launch_bounds__(32 * W) leg_inv_tma_kernel(int R, int J, int Jp, int nlat, int nq, int nct,
+                                                            const double* __restrict__ ptab,
+                                                            const int* __restrict__ cbase,
+                                                            const double* __restrict__ Xt,
+                                                            double2* __restrict__ out) {
+    constexpr int SX = 8 * NT + 2;
+    constexpr unsigned PB = 32 * 16 * sizeof(double);
+    constexpr unsigned XB = CH * SX * sizeof(double);
+    extern __shared__ __align__(128) double smem[];
+    double* sP = smem;                        // [S][W][32 * 16]
+    double* sX = sP + S * W * 512;            // [S][CH * SX]
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(sX + S * CH * SX);
+    unsigned long long* empty = full + S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = blockIdx.y;
     const int len = R + 2 - m;
     const int nch = (len + CH - 1) / CH;
-    const int sl = blockIdx.x * W + warp;
-    double* tiles = smem + warp * (2 * 32 * ST + 2 * CH * SX);  // [2][32][ST] then [2][CH][SX]
-    double* xs = tiles + 2 * 32 * ST;
-    const int q0 = blockIdx.z * NQ;
-    const long Kq = EXT ? (long)(R + 1) * (R + 4) / 2 : (long)(R + 1) * (R + 2) / 2;
-    const long base = EXT ? off_ext(R, m) : off_std(R, m);
-    const int tlim = EXT ? len : len - 1;
-    if (sl * 32 >= Jp) return;
-    const double* __restrict__ pm = ptab + (long)cbase[m] * Jp * 16 + (long)sl * 32 * 16;
+    const int nsl = Jp >> 5;
+    const int sl0 = blockIdx.x * W;
+    const int nact = min(W, nsl - sl0);
+    const int z = blockIdx.z;
+    const int q0 = z * 4 * NT;
+    const double* __restrict__ pm = ptab + (long)cbase[m] * Jp * 16 + (long)sl0 * 512;
+    const double* __restrict__ xm = Xt + ((long)z * nct + cbase[m]) * CH * SX;
     const int r4 = lane >> 2, c4 = lane & 3;
 
-    // X chunk: 16 degrees x NQ complex columns -> xs[tl][2 ql + v], zero beyond tlim / nq
-    // asynchronous (cp.async, zero-filled) so it overlaps the DMMAs of the previous chunk
-    auto stage_x = [&](double* dst, int t0) {
-        for (int idx = lane; idx < CH * NQ; idx += 32) {
-            const int ql = idx / CH, tl = idx - ql * CH;  // degree fastest
-            const int t = t0 + tl, q = q0 + ql;
-            const bool v = t < tlim && q < nq;
-            legc::cp_async16z(dst + tl * SX + 2 * ql, v ? (const void*)(X + (long)q * Kq + base + t) : (const void*)X, v);
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < S; ++k) {
+            mbar_init(full + k, 1);
+            mbar_init(empty + k, W);
         }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int c) {
+        const int k = c % S;
+        mbar_expect_tx(full + k, nact * PB + XB);
+        for (int w = 0; w < nact; ++w)
+            bulk_g2s(sP + (k * W + w) * 512, pm + (long)c * Jp * 16 + w * 512, PB, full + k);
+        bulk_g2s(sX + k * CH * SX, xm + (long)c * CH * SX, XB, full + k);
     };
+    if (threadIdx.x == 0)
+        for (int c = 0; c < S && c < nch; ++c) issue(c);
 
     double acc[4][2][NT][2];
 #pragma unroll
@@ -224,40 +328,40 @@ __global__ void __launch_bounds__(256) leg_inv_stream_mma_kernel(int R, int J, i
 #pragma unroll
             for (int cc = 0; cc < NT; ++cc) acc[a][b][cc][0] = acc[a][b][cc][1] = 0.0;
 
-    load_tile(tiles, pm, lane);
-    stage_x(xs, 0);
-    cp_async_commit();
     for (int c = 0; c < nch; ++c) {
-        const int b = c & 1;
-        if (c + 1 < nch) {
-            load_tile(tiles + (b ^ 1) * 32 * ST, pm + (long)(c + 1) * Jp * 16, lane);
-            stage_x(xs + (b ^ 1) * CH * SX, (c + 1) * CH);
-        }
-        cp_async_commit();
-        cp_async_wait<1>();
+        const int k = c % S;
+        const unsigned ph = (unsigned)(c / S) & 1u;
+        mbar_wait(full + k, ph);
         __syncwarp();
-        const double* tl = tiles + b * 32 * ST;
-        const double* xb = xs + b * CH * SX;
+        if (warp < nact) {
+            const double* tl = sP + (k * W + warp) * 512;
+            const double* xb = sX + k * CH * SX;
 #pragma unroll
-        for (int par = 0; par < 2; ++par) {
+            for (int par = 0; par < 2; ++par) {
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-                // k -> degree (within chunk) par + 2 (4 ks + c4)
-                double bf[NT], af[4];
+                for (int ks = 0; ks < 2; ++ks) {
+                    // k -> degree (within chunk) par + 2 (4 ks + c4)
+                    double bf[NT], af[4];
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) bf[nt] = xb[(par + 2 * (4 * ks + c4)) * SX + 8 * nt + r4];
+                    for (int nt = 0; nt < NT; ++nt) bf[nt] = xb[(par + 2 * (4 * ks + c4)) * SX + 8 * nt + r4];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) af[mt] = tl[(8 * mt + r4) * ST + par * 8 + 4 * ks + c4];
+                    for (int mt = 0; mt < 4; ++mt) af[mt] = tl[(8 * mt + r4) * 16 + pswz(r4, par * 8 + 4 * ks + c4)];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt)
+                    for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][par][nt], af[mt], bf[nt]);
+                        for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][par][nt], af[mt], bf[nt]);
+                }
             }
         }
         __syncwarp();
+        if (lane == 0) mbar_arrive(empty + k);
+        if (threadIdx.x == 0 && c + S < nch) {
+            mbar_wait(empty + k, ph);
+            issue(c + S);
+        }
     }
-    cp_async_wait<0>();
-    const int jb = sl * 32;
+    if (warp >= nact) return;
+    const int jb = (sl0 + warp) * 32;
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
         const int jj = jb + 8 * mt + r4;
@@ -285,7 +389,7 @@ void fwd_launch(const pswe_plan& P, const double2* four, int nq, double2* out, b
     const int W = w_env > 0 ? w_env : (P.J <= 256 ? 4 : 8);
     const int Jp = ((P.J + 31) / 32) * 32;
     const int groups = (nq + 4 * NT - 1) / (4 * NT);
-    const size_t sm = (size_t)(2 * Jp * 8 * NT + W * 2 * 32 * ST) * sizeof(double);
+    const size_t sm = (size_t)(2 * Jp * 8 * NT + W * 2 * 32 * 16) * sizeof(double);
     if (sm > 227 * 1024) throw std::invalid_argument("legendre_forward(stream): shared-memory tile too large");
     auto kern = leg_fwd_stream_mma_kernel<NT>;
     if (sm > 48 * 1024) PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -294,49 +398,42 @@ void fwd_launch(const pswe_plan& P, const double2* four, int nq, double2* out, b
     PSWE_LAUNCH_CHECK();
 }
 
-template <bool EXT, int NT>
-void inv_launch(const pswe_plan& P, const double2* X, int nq, double2* out, cudaStream_t st) {
-    const int nsl = (P.J + 31) / 32;
-    const int Jp = nsl * 32;
-    const int W = nsl < 4 ? nsl : 4;
-    const int groups = (nq + 4 * NT - 1) / (4 * NT);
-    const size_t sm = (size_t)W * (2 * 32 * ST + 2 * CH * (8 * NT + 2)) * sizeof(double);
-    auto kern = leg_inv_stream_mma_kernel<EXT, NT>;
-    if (sm > 48 * 1024) PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    kern<<<dim3((nsl + W - 1) / W, P.R + 1, groups), 32 * W, sm, st>>>(P.R, P.J, Jp, P.nlat, nq, P.d_ptab2,
-                                                                       P.d_chk_off, X, out);
-    PSWE_LAUNCH_CHECK();
-}
+constexpr int kInvStages = 4;
 
-template <bool EXT>
-void inv_dispatch(const pswe_plan& P, const double2* X, int nq, double2* out, cudaStream_t st) {
-    // cost per (chunk, slice) in shared-memory wavefronts + DMMA issue: a block of NT n-tiles
-    // issues 16 NT DMMA (x16 cycles) against 16 P-fragment + 4 NT X-fragment loads (2 wavefronts
-    // each, shared by the SM's 4 SMSPs), plus one P tile (32 wavefronts) per column group.
-    // Measured (tools/stage_times.py): NT = 5 (one group of 20 columns: 0.45 fragment loads per
-    // DMMA, 252 registers) wins for a 5-state batch once there are >= 192 latitude pairs to fill
-    // the machine; otherwise the fewest padded n-tiles, then the fewest groups.
-    int best = 1;
-    if (nq >= 20 && nq % 20 == 0 && P.J >= 192) {
-        best = 5;
-    } else {
-        int best_cost = 1 << 30;
-        for (int nt = 4; nt >= 1; --nt) {
-            const int groups = (nq + 4 * nt - 1) / (4 * nt);
-            const int cost = groups * nt * 8 + groups;
-            if (cost < best_cost) {
-                best_cost = cost;
-                best = nt;
-            }
+// column tiles per group for nq complex columns. Measured (tools/stage_times.py): NT = 5 (one
+// group of 20 columns, 0.45 fragment loads per DMMA) wins for a 5-state batch once there are
+// >= 192 latitude pairs to fill the machine; otherwise the fewest padded n-tiles, then the fewest
+// groups (each group re-streams the P table).
+int inv_choose_nt(const pswe_plan& P, int nq) {
+    if (nq >= 20 && nq % 20 == 0 && P.J >= 192) return 5;
+    int best = 1, best_cost = 1 << 30;
+    for (int nt = 4; nt >= 1; --nt) {
+        const int groups = (nq + 4 * nt - 1) / (4 * nt);
+        const int cost = groups * nt * 8 + groups;
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = nt;
         }
     }
-    switch (best) {
-        case 5: inv_launch<EXT, 5>(P, X, nq, out, st); break;
-        case 4: inv_launch<EXT, 4>(P, X, nq, out, st); break;
-        case 3: inv_launch<EXT, 3>(P, X, nq, out, st); break;
-        case 2: inv_launch<EXT, 2>(P, X, nq, out, st); break;
-        default: inv_launch<EXT, 1>(P, X, nq, out, st); break;
+    return best;
+}
+
+template <int NT>
+void inv_tma_launch(const pswe_plan& P, const double* Xt, int nq, double2* out, cudaStream_t st) {
+    constexpr int W = 2, S = kInvStages;
+    const int nsl = (P.J + 31) / 32;
+    const int Jp = nsl * 32;
+    const int groups = (nq + 4 * NT - 1) / (4 * NT);
+    const size_t sm = (size_t)S * (W * 512 + CH * (8 * NT + 2)) * sizeof(double) + 2 * S * sizeof(unsigned long long);
+    auto kern = leg_inv_tma_kernel<NT, W, S>;
+    static bool attr = false;
+    if (!attr) {
+        PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr = true;
     }
+    kern<<<dim3((nsl + W - 1) / W, P.R + 1, groups), 32 * W, sm, st>>>(P.R, P.J, Jp, P.nlat, nq, P.n_chunks,
+                                                                       P.d_ptab2, P.d_chk_off, Xt, out);
+    PSWE_LAUNCH_CHECK();
 }
 
 }  // namespace
@@ -349,6 +446,12 @@ void build_legendre_table2(pswe_plan& P) {
     for (int m = 0; m <= P.R; ++m) off[m + 1] = off[m] + (P.R + 2 - m + CH - 1) / CH;
     const size_t n = (size_t)off[P.R + 1] * Jp * 16;
     PSWE_CUDA(cudaMalloc(&P.d_ptab2, n * sizeof(double)));
+    P.n_chunks = off[P.R + 1];
+    std::vector<int> cm(P.n_chunks);
+    for (int m = 0; m <= P.R; ++m)
+        for (int c = off[m]; c < off[m + 1]; ++c) cm[c] = m;
+    PSWE_CUDA(cudaMalloc(&P.d_chunk_m, cm.size() * sizeof(int)));
+    PSWE_CUDA(cudaMemcpy(P.d_chunk_m, cm.data(), cm.size() * sizeof(int), cudaMemcpyHostToDevice));
     dim3 grid((Jp + 127) / 128, P.R + 1);
     build_ptab2_kernel<<<grid, 128>>>(P.R, P.J, Jp, P.d_mu_n, P.d_seed, P.d_rec, P.d_chk_off, P.d_ptab2);
     PSWE_LAUNCH_CHECK();
@@ -361,12 +464,38 @@ void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, do
     else fwd_launch<1>(P, four, nq, out, ext, st);
 }
 
-// kind/nq as legendre_inverse_mma; X = prep output (UV/EVAL, ext layout) or input fields (PLAIN)
-void legendre_inverse_stream(const pswe_plan& P, bool ext_layout, const double2* X, int nq, double2* out,
-                             cudaStream_t st) {
+// kind/nq/in/in2/radius as legendre_inverse_mma: tiled prep, then the TMA-pipelined contraction.
+void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq,
+                             double radius, double2* out, cudaStream_t st) {
     if (nq <= 0) return;
-    if (ext_layout) inv_dispatch<true>(P, X, nq, out, st);
-    else inv_dispatch<false>(P, X, nq, out, st);
+    const int NT = inv_choose_nt(P, nq);
+    const int NQ = 4 * NT, SX = 8 * NT + 2;
+    const int groups = (nq + NQ - 1) / NQ;
+    const size_t need = (size_t)groups * P.n_chunks * CH * SX;
+    if (need > P.xtile_cap) {
+        if (P.d_xtile) PSWE_CUDA(cudaFree(P.d_xtile));
+        PSWE_CUDA(cudaMalloc(&P.d_xtile, need * sizeof(double)));
+        P.xtile_cap = need;
+    }
+    dim3 g(P.n_chunks, groups);
+    const int nthr = CH * NQ;
+    if (kind == INV_EVAL)
+        xtile_prep_kernel<INV_EVAL><<<g, nthr, 0, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
+                                                        P.d_eps, in, in2, radius, P.d_xtile);
+    else if (kind == INV_UV)
+        xtile_prep_kernel<INV_UV><<<g, nthr, 0, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
+                                                      P.d_eps, in, in2, radius, P.d_xtile);
+    else
+        xtile_prep_kernel<INV_PLAIN><<<g, nthr, 0, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
+                                                         P.d_eps, in, in2, radius, P.d_xtile);
+    PSWE_LAUNCH_CHECK();
+    switch (NT) {
+        case 5: inv_tma_launch<5>(P, P.d_xtile, nq, out, st); break;
+        case 4: inv_tma_launch<4>(P, P.d_xtile, nq, out, st); break;
+        case 3: inv_tma_launch<3>(P, P.d_xtile, nq, out, st); break;
+        case 2: inv_tma_launch<2>(P, P.d_xtile, nq, out, st); break;
+        default: inv_tma_launch<1>(P, P.d_xtile, nq, out, st); break;
+    }
 }
 
 }  // namespace pswe

@@ -135,13 +135,27 @@ void pswe_plan::reserve(int batch) {
     PSWE_CUDA(cudaMalloc(&d_four_b, four * sizeof(double2)));
     PSWE_CUDA(cudaMalloc(&d_proj, (size_t)batch * 5 * Kx * sizeof(double2)));
     PSWE_CUDA(cudaMalloc(&d_xcoef, (size_t)batch * 5 * Kx * sizeof(double2)));
+    if (n_chunks > 0) {  // STREAM inverse X tiles for up to 5 batch columns, any column tiling
+        const int nq = 5 * batch;
+        size_t need = 0;
+        for (int nt = 1; nt <= 5; ++nt) {
+            const size_t d = (size_t)((nq + 4 * nt - 1) / (4 * nt)) * (8 * nt + 2) * n_chunks * 16;
+            need = d > need ? d : need;
+        }
+        if (need > xtile_cap) {
+            if (d_xtile) cudaFree(d_xtile);
+            d_xtile = nullptr;
+            PSWE_CUDA(cudaMalloc(&d_xtile, need * sizeof(double)));
+            xtile_cap = need;
+        }
+    }
     cap_batch = batch;
 }
 
 static void plan_free(pswe_plan* p) {
     void* ptrs[] = {p->d_mu_n, p->d_seed, p->d_rec, p->d_eps, p->d_ptab, p->d_rowc, p->d_roww,
                     p->d_rowmu, p->d_fft_tw, p->d_fft_post, p->d_four_a, p->d_four_b, p->d_proj,
-                    p->d_xcoef, p->d_chk, p->d_chk_off, p->d_fft_roots, p->d_fft_ptw, p->d_fft_iptw, p->d_ptab2};
+                    p->d_xcoef, p->d_chk, p->d_chk_off, p->d_fft_roots, p->d_fft_ptw, p->d_fft_iptw, p->d_ptab2, p->d_chunk_m, p->d_xtile};
     for (void* q : ptrs)
         if (q) cudaFree(q);
 }

@@ -89,7 +89,11 @@ struct pswe_plan {
     double* d_ptab = nullptr;    // STREAM mode: [Kx * J] P^m_s(mu_j), block m: [j][s]
     double2* d_chk = nullptr;    // [sum_m ceil((R+2-m)/16)][J] (P_t, P_{t-1}) at t = 16c (forward DMMA)
     int* d_chk_off = nullptr;    // [R+2] chunk offsets per m into d_chk
-    double* d_ptab2 = nullptr;   // STREAM mode: P tiles [m][chunk][Jp][par][8] (legendre_stream.cu)
+    double* d_ptab2 = nullptr;   // STREAM mode: P tiles [m][chunk][Jp][16] swizzled (legendre_stream.cu)
+    int n_chunks = 0;            // STREAM mode: 16-degree chunks over all m (= d_chk_off[R+1])
+    int* d_chunk_m = nullptr;    // STREAM mode: [n_chunks] order m of each chunk
+    mutable double* d_xtile = nullptr;  // STREAM mode: inverse X tiles (grow-only scratch)
+    mutable size_t xtile_cap = 0;       // doubles
     double* d_rowc = nullptr;    // [nlat] cos(phi_i)
     double* d_roww = nullptr;    // [nlat] Gauss weight w_i
     double* d_rowmu = nullptr;   // [nlat] mu_i
@@ -131,8 +135,8 @@ void build_legendre_checkpoints(pswe_plan& P);
 void build_legendre_table2(pswe_plan& P);
 void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
                              cudaStream_t st);
-void legendre_inverse_stream(const pswe_plan& P, bool ext_layout, const double2* X, int nq, double2* out,
-                             cudaStream_t st);
+void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq,
+                             double radius, double2* out, cudaStream_t st);
 
 // fft.cu
 // Fourier rows [b][m][i] -> grid [b][i][j] (c2r, Im G_0 := 0), optional per-row 1/cos(phi).
