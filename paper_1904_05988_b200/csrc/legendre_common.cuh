@@ -12,10 +12,12 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
         : "d"(a), "d"(b));
 }
 
-// -a^2/(s(s+1)) x_s (inverse Laplacian at degree s of order m; 0 outside m..R and at s = 0)
-__device__ __forceinline__ double2 inv_lap_at(const double2* __restrict__ x, long bs, int m, int R, int t, double a2) {
+// -a^2/(s(s+1)) x_s (inverse Laplacian at degree s of order m; 0 outside m..R and at s = 0);
+// with rtab (rtab[s] = 1/(s(s+1)), host-rounded) the division becomes one multiply
+__device__ __forceinline__ double2 inv_lap_at(const double2* __restrict__ x, long bs, int m, int R, int t, double a2,
+                                              const double* __restrict__ rtab = nullptr) {
     if (t < m || t > R || t == 0) return make_double2(0.0, 0.0);
-    const double f = -a2 / (t * (t + 1.0));
+    const double f = rtab ? -a2 * __ldg(rtab + t) : -a2 / (t * (t + 1.0));
     const double2 v = x[bs + t - m];
     return make_double2(v.x * f, v.y * f);
 }
@@ -23,16 +25,17 @@ __device__ __forceinline__ double2 inv_lap_at(const double2* __restrict__ x, lon
 // H-sum coefficient at degree t rewritten as a P-sum over one extra degree:
 // c_t = -(t-1) eps_t psi_{t-1} + (t+2) eps_{t+1} psi_{t+1}, psi = inverse Laplacian of x
 __device__ __forceinline__ double2 hcoef(const double2* __restrict__ x, const double* __restrict__ eps, long bs,
-                                         long bx, int m, int R, int t, double a2) {
+                                         long bx, int m, int R, int t, double a2,
+                                         const double* __restrict__ rtab = nullptr) {
     double2 c = make_double2(0.0, 0.0);
     if (t - 1 >= m) {
-        const double2 pm = inv_lap_at(x, bs, m, R, t - 1, a2);
+        const double2 pm = inv_lap_at(x, bs, m, R, t - 1, a2, rtab);
         const double f = -(double)(t - 1) * eps[bx + t - m];
         c.x += f * pm.x;
         c.y += f * pm.y;
     }
     if (t + 1 <= R) {
-        const double2 pp = inv_lap_at(x, bs, m, R, t + 1, a2);
+        const double2 pp = inv_lap_at(x, bs, m, R, t + 1, a2, rtab);
         const double f = (double)(t + 2) * eps[bx + t + 1 - m];
         c.x += f * pp.x;
         c.y += f * pp.y;

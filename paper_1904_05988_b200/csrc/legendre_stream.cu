@@ -216,86 +216,103 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
 // X tiles: per column group z (4 NT complex columns from q0 = 4 NT z), per chunk (cbase(m) + c):
 // [16 degrees tl][8 NT + 2] doubles, column 2 ql + {re, im}, two zero pad columns; degree
 // t = 16 c + tl of order m (extended t = 0..R+1-m; standard t = 0..R-m), zero beyond.
-// prep: thread (tl, ql) of block (chunk, z) computes one complex entry (transform.cpp:204-206
-// with the H-sums as P-sums): EVAL q = 4 state + {Phi, zeta, U, V}, UV q = 2 pair + {U, V},
-// PLAIN q = field (standard layout, copied).
+// prep: block (chunk, z), thread (item bl, degree tl) with the degree fastest (coalesced reads
+// of the m-major coefficient rows) computes all PER columns of its item (transform.cpp:204-206
+// with the H-sums as P-sums): EVAL item = state, columns {Phi, zeta, U, V}; UV item = pair,
+// columns {U, V}; PLAIN item = field (standard layout, copied). The tile is assembled in shared
+// memory and stored as one contiguous block.
 template <int KIND>
 __global__ void xtile_prep_kernel(int R, int NQ, int SX, int nq, int nct, const int* __restrict__ chunk_m,
                                   const int* __restrict__ cbase, const double* __restrict__ eps,
-                                  const double2* __restrict__ in, const double2* __restrict__ in2, double radius,
-                                  double* __restrict__ Xt) {
+                                  const double* __restrict__ rtab, const double2* __restrict__ in,
+                                  const double2* __restrict__ in2, double radius, double* __restrict__ Xt) {
+    constexpr int PER = KIND == INV_EVAL ? 4 : (KIND == INV_UV ? 2 : 1);
+    extern __shared__ double tile[];  // [CH][SX]
     const int cg = blockIdx.x, z = blockIdx.y;
-    const int ql = threadIdx.x % NQ, tl = threadIdx.x / NQ;
+    const int tl = threadIdx.x & (CH - 1), bl = threadIdx.x / CH;
     const int m = chunk_m[cg];
     const int t = (cg - cbase[m]) * CH + tl;
     const int s = m + t;
-    const int q = z * NQ + ql;
+    const int item = (z * NQ) / PER + bl;
     const long K = (long)(R + 1) * (R + 2) / 2;
     const long bs = off_std(R, m), bx = off_ext(R, m);
-    double2 v = make_double2(0.0, 0.0);
-    if (q < nq) {
+    double2 v[PER];
+#pragma unroll
+    for (int f = 0; f < PER; ++f) v[f] = make_double2(0.0, 0.0);
+    if (bl * PER < NQ && item * PER < nq) {
         if (KIND == INV_PLAIN) {
-            if (s <= R) v = in[(long)q * K + bs + t];
+            if (s <= R) v[0] = in[(long)item * K + bs + t];
         } else if (s <= R + 1) {
             const double a2 = radius * radius, inv_a = 1.0 / radius;
-            int f;
             const double2 *vort, *div;
+            int o = 0;
             if (KIND == INV_EVAL) {
-                const int b = q >> 2;
-                f = q & 3;
-                const double2* st = in + (long)b * 3 * K;
+                const double2* st = in + (long)item * 3 * K;
                 vort = st + K;
                 div = st + 2 * K;
-                if (f < 2) {
-                    if (s <= R) v = (f == 0 ? st : vort)[bs + t];
-                    f = -1;
+                if (s <= R) {
+                    v[0] = st[bs + t];
+                    v[1] = vort[bs + t];
                 }
+                o = 2;
             } else {
-                const int pr = q >> 1;
-                f = 2 + (q & 1);
-                vort = in + (long)pr * K;
-                div = in2 + (long)pr * K;
+                vort = in + (long)item * K;
+                div = in2 + (long)item * K;
             }
-            if (f == 2) {
-                const double2 chi = legc::inv_lap_at(div, bs, m, R, s, a2);
-                const double2 cpsi = legc::hcoef(vort, eps, bs, bx, m, R, s, a2);
-                v = make_double2(inv_a * (-m * chi.y - cpsi.x), inv_a * (m * chi.x - cpsi.y));
-            } else if (f == 3) {
-                const double2 psi = legc::inv_lap_at(vort, bs, m, R, s, a2);
-                const double2 cchi = legc::hcoef(div, eps, bs, bx, m, R, s, a2);
-                v = make_double2(inv_a * (-m * psi.y + cchi.x), inv_a * (m * psi.x + cchi.y));
-            }
+            const double2 chi = legc::inv_lap_at(div, bs, m, R, s, a2, rtab);
+            const double2 cpsi = legc::hcoef(vort, eps, bs, bx, m, R, s, a2, rtab);
+            const double2 psi = legc::inv_lap_at(vort, bs, m, R, s, a2, rtab);
+            const double2 cchi = legc::hcoef(div, eps, bs, bx, m, R, s, a2, rtab);
+            v[o] = make_double2(inv_a * (-m * chi.y - cpsi.x), inv_a * (m * chi.x - cpsi.y));
+            v[o + 1] = make_double2(inv_a * (-m * psi.y + cchi.x), inv_a * (m * psi.x + cchi.y));
         }
     }
-    double* row = Xt + ((long)z * nct + cg) * CH * SX + (long)tl * SX;
-    *reinterpret_cast<double2*>(row + 2 * ql) = v;
-    if (ql == 0) *reinterpret_cast<double2*>(row + 2 * NQ) = make_double2(0.0, 0.0);
+    if (bl * PER < NQ) {
+#pragma unroll
+        for (int f = 0; f < PER; ++f) {
+            tile[tl * SX + 2 * (bl * PER + f)] = v[f].x;
+            tile[tl * SX + 2 * (bl * PER + f) + 1] = v[f].y;
+        }
+    }
+    if (threadIdx.x < CH) {
+        tile[threadIdx.x * SX + 2 * NQ] = 0.0;
+        tile[threadIdx.x * SX + 2 * NQ + 1] = 0.0;
+    }
+    __syncthreads();
+    double2* dst = reinterpret_cast<double2*>(Xt + ((long)z * nct + cg) * CH * SX);
+    const double2* src = reinterpret_cast<const double2*>(tile);
+    for (int i = threadIdx.x; i < CH * SX / 2; i += blockDim.x) dst[i] = src[i];
 }
 
-// grid (ceil(nslices / W), R+1, column groups); warp = 32-latitude slice walking all chunks of
-// its m; an S-stage ring of {W P tiles, one X tile} per block, filled by bulk copies issued by
-// thread 0 (full[s]: expect_tx + complete_tx) and released by one arrival per warp (empty[s]).
-template <int NT, int W, int S>
-__global__ void __launch_bounds__(32 * W) leg_inv_tma_kernel(int R, int J, int Jp, int nlat, int nq, int nct,
-                                                            const double* __restrict__ ptab,
-                                                            const int* __restrict__ cbase,
-                                                            const double* __restrict__ Xt,
-                                                            double2* __restrict__ out) {
+// grid (ceil(nslices / WS), R+1, column groups); 2 WS warps per block: warps 2w, 2w+1 share
+// latitude slice WS blockIdx.x + w and take its latitudes 0-15 / 16-31 (two 8-row m-tiles each)
+// over all chunks of the order m. Halving the per-warp unit (vs one warp per slice) keeps the
+// longest tasks (m = 0) below the per-SM average and halves the accumulators (more resident
+// warps); the P and X tiles of a stage are shared by all warps of the block. An S-stage ring of
+// {WS P tiles, one X tile} per chunk is filled by bulk copies from thread 0 (full[s]: expect_tx +
+// complete_tx) and released by one arrival per warp (empty[s]).
+template <int NT, int S, int WS>
+__global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int Jp, int nlat, int nq, int nct,
+                                                             const double* __restrict__ ptab,
+                                                             const int* __restrict__ cbase,
+                                                             const double* __restrict__ Xt,
+                                                             double2* __restrict__ out) {
     constexpr int SX = 8 * NT + 2;
     constexpr unsigned PB = 32 * 16 * sizeof(double);
     constexpr unsigned XB = CH * SX * sizeof(double);
     extern __shared__ __align__(128) double smem[];
-    double* sP = smem;                        // [S][W][32 * 16]
-    double* sX = sP + S * W * 512;            // [S][CH * SX]
+    double* sP = smem;                 // [S][WS][32 * 16]
+    double* sX = sP + S * WS * 512;    // [S][CH * SX]
     unsigned long long* full = reinterpret_cast<unsigned long long*>(sX + S * CH * SX);
     unsigned long long* empty = full + S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ws = warp >> 1, mh = warp & 1;
     const int m = blockIdx.y;
     const int len = R + 2 - m;
     const int nch = (len + CH - 1) / CH;
     const int nsl = Jp >> 5;
-    const int sl0 = blockIdx.x * W;
-    const int nact = min(W, nsl - sl0);
+    const int sl0 = blockIdx.x * WS;
+    const int nact = min(WS, nsl - sl0);
     const int z = blockIdx.z;
     const int q0 = z * 4 * NT;
     const double* __restrict__ pm = ptab + (long)cbase[m] * Jp * 16 + (long)sl0 * 512;
@@ -305,7 +322,7 @@ __global__ void __launch_bounds__(32 * W) leg_inv_tma_kernel(int R, int J, int J
     if (threadIdx.x == 0) {
         for (int k = 0; k < S; ++k) {
             mbar_init(full + k, 1);
-            mbar_init(empty + k, W);
+            mbar_init(empty + k, 2 * WS);
         }
         mbar_fence_init();
     }
@@ -314,15 +331,17 @@ __global__ void __launch_bounds__(32 * W) leg_inv_tma_kernel(int R, int J, int J
         const int k = c % S;
         mbar_expect_tx(full + k, nact * PB + XB);
         for (int w = 0; w < nact; ++w)
-            bulk_g2s(sP + (k * W + w) * 512, pm + (long)c * Jp * 16 + w * 512, PB, full + k);
+            bulk_g2s(sP + (k * WS + w) * 512, pm + (long)c * Jp * 16 + w * 512, PB, full + k);
         bulk_g2s(sX + k * CH * SX, xm + (long)c * CH * SX, XB, full + k);
     };
+#ifndef PSWE_DIAG_NOTMA
     if (threadIdx.x == 0)
         for (int c = 0; c < S && c < nch; ++c) issue(c);
+#endif
 
-    double acc[4][2][NT][2];
+    double acc[2][2][NT][2];  // [m-tile 2 mh + a][parity][n-tile][v]
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int b = 0; b < 2; ++b)
 #pragma unroll
@@ -331,48 +350,61 @@ __global__ void __launch_bounds__(32 * W) leg_inv_tma_kernel(int R, int J, int J
     for (int c = 0; c < nch; ++c) {
         const int k = c % S;
         const unsigned ph = (unsigned)(c / S) & 1u;
+#ifndef PSWE_DIAG_NOTMA
         mbar_wait(full + k, ph);
+#endif
         __syncwarp();
-        if (warp < nact) {
-            const double* tl = sP + (k * W + warp) * 512;
+        if (ws < nact) {
+            const double* tl = sP + (k * WS + ws) * 512 + mh * 16 * 16;  // this warp's 16 latitude rows
             const double* xb = sX + k * CH * SX;
 #pragma unroll
             for (int par = 0; par < 2; ++par) {
 #pragma unroll
                 for (int ks = 0; ks < 2; ++ks) {
                     // k -> degree (within chunk) par + 2 (4 ks + c4)
-                    double bf[NT], af[4];
+                    double bf[NT], af[2];
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) bf[nt] = xb[(par + 2 * (4 * ks + c4)) * SX + 8 * nt + r4];
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) af[mt] = tl[(8 * mt + r4) * 16 + pswz(r4, par * 8 + 4 * ks + c4)];
+                    for (int a = 0; a < 2; ++a) af[a] = tl[(8 * a + r4) * 16 + pswz(r4, par * 8 + 4 * ks + c4)];
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt)
+                    for (int a = 0; a < 2; ++a)
 #pragma unroll
-                        for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][par][nt], af[mt], bf[nt]);
+                        for (int nt = 0; nt < NT; ++nt) {
+#ifdef PSWE_DIAG_NODMMA
+                            acc[a][par][nt][0] += af[a] * bf[nt];
+#else
+                            dmma(acc[a][par][nt], af[a], bf[nt]);
+#endif
+                        }
                 }
             }
         }
         __syncwarp();
+#ifndef PSWE_DIAG_NOTMA
         if (lane == 0) mbar_arrive(empty + k);
         if (threadIdx.x == 0 && c + S < nch) {
             mbar_wait(empty + k, ph);
             issue(c + S);
         }
+#endif
     }
-    if (warp >= nact) return;
-    const int jb = (sl0 + warp) * 32;
+    if (ws >= nact) return;
+    const int jb = (sl0 + ws) * 32 + mh * 16;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-        const int jj = jb + 8 * mt + r4;
+    for (int a = 0; a < 2; ++a) {
+        const int jj = jb + 8 * a + r4;
         if (jj >= J) continue;
         const int iN = nlat - J + jj, iS = J - 1 - jj;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
             const int q = q0 + 4 * nt + c4;
             if (q >= nq) continue;
-            const double* e = acc[mt][0][nt];
-            const double* o = acc[mt][1][nt];
+            const double* e = acc[a][0][nt];
+            const double* o = acc[a][1][nt];
+#ifdef PSWE_DIAG_NOSTORE
+            if (e[0] != 1.2345e300) continue;
+#endif
             double2* dst = out + (long)q * nlat * (R + 1) + m;  // rows [q][i][m]
             dst[(long)iN * (R + 1)] = make_double2(e[0] + o[0], e[1] + o[1]);
             if (iS != iN) dst[(long)iS * (R + 1)] = make_double2(e[0] - o[0], e[1] - o[1]);
@@ -398,7 +430,14 @@ void fwd_launch(const pswe_plan& P, const double2* four, int nq, double2* out, b
     PSWE_LAUNCH_CHECK();
 }
 
-constexpr int kInvStages = 4;
+#ifndef PSWE_INV_STAGES
+#define PSWE_INV_STAGES 4
+#endif
+#ifndef PSWE_INV_SLICES
+#define PSWE_INV_SLICES 2
+#endif
+constexpr int kInvStages = PSWE_INV_STAGES;  // ring stages (one chunk each)
+constexpr int kInvSlices = PSWE_INV_SLICES;  // latitude slices per block (two warps each)
 
 // column tiles per group for nq complex columns. Measured (tools/stage_times.py): NT = 5 (one
 // group of 20 columns, 0.45 fragment loads per DMMA) wins for a 5-state batch once there are
@@ -420,19 +459,19 @@ int inv_choose_nt(const pswe_plan& P, int nq) {
 
 template <int NT>
 void inv_tma_launch(const pswe_plan& P, const double* Xt, int nq, double2* out, cudaStream_t st) {
-    constexpr int W = 2, S = kInvStages;
+    constexpr int S = kInvStages, WS = kInvSlices;
     const int nsl = (P.J + 31) / 32;
     const int Jp = nsl * 32;
     const int groups = (nq + 4 * NT - 1) / (4 * NT);
-    const size_t sm = (size_t)S * (W * 512 + CH * (8 * NT + 2)) * sizeof(double) + 2 * S * sizeof(unsigned long long);
-    auto kern = leg_inv_tma_kernel<NT, W, S>;
+    const size_t sm = (size_t)S * (WS * 512 + CH * (8 * NT + 2)) * sizeof(double) + 2 * S * sizeof(unsigned long long);
+    auto kern = leg_inv_tma_kernel<NT, S, WS>;
     static bool attr = false;
     if (!attr) {
         PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr = true;
     }
-    kern<<<dim3((nsl + W - 1) / W, P.R + 1, groups), 32 * W, sm, st>>>(P.R, P.J, Jp, P.nlat, nq, P.n_chunks,
-                                                                       P.d_ptab2, P.d_chk_off, Xt, out);
+    kern<<<dim3((nsl + WS - 1) / WS, P.R + 1, groups), 64 * WS, sm, st>>>(P.R, P.J, Jp, P.nlat, nq, P.n_chunks,
+                                                                           P.d_ptab2, P.d_chk_off, Xt, out);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -478,17 +517,25 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
         P.xtile_cap = need;
     }
     dim3 g(P.n_chunks, groups);
-    const int nthr = CH * NQ;
+    const int per = kind == INV_EVAL ? 4 : (kind == INV_UV ? 2 : 1);
+    const int nthr = CH * ((NQ + per - 1) / per);
+    const size_t tsm = (size_t)CH * SX * sizeof(double);
+#ifdef PSWE_DIAG_NOPREP
+    if (false)
+#endif
     if (kind == INV_EVAL)
-        xtile_prep_kernel<INV_EVAL><<<g, nthr, 0, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
-                                                        P.d_eps, in, in2, radius, P.d_xtile);
+        xtile_prep_kernel<INV_EVAL><<<g, nthr, tsm, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
+                                                          P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     else if (kind == INV_UV)
-        xtile_prep_kernel<INV_UV><<<g, nthr, 0, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
-                                                      P.d_eps, in, in2, radius, P.d_xtile);
+        xtile_prep_kernel<INV_UV><<<g, nthr, tsm, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
+                                                        P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     else
-        xtile_prep_kernel<INV_PLAIN><<<g, nthr, 0, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
-                                                         P.d_eps, in, in2, radius, P.d_xtile);
+        xtile_prep_kernel<INV_PLAIN><<<g, nthr, tsm, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
+                                                           P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     PSWE_LAUNCH_CHECK();
+#ifdef PSWE_DIAG_NOINV
+    return;
+#endif
     switch (NT) {
         case 5: inv_tma_launch<5>(P, P.d_xtile, nq, out, st); break;
         case 4: inv_tma_launch<4>(P, P.d_xtile, nq, out, st); break;

@@ -153,7 +153,7 @@ void pswe_plan::reserve(int batch) {
 }
 
 static void plan_free(pswe_plan* p) {
-    void* ptrs[] = {p->d_mu_n, p->d_seed, p->d_rec, p->d_eps, p->d_ptab, p->d_rowc, p->d_roww,
+    void* ptrs[] = {p->d_mu_n, p->d_seed, p->d_rec, p->d_eps, p->d_rlap, p->d_ptab, p->d_rowc, p->d_roww,
                     p->d_rowmu, p->d_fft_tw, p->d_fft_post, p->d_four_a, p->d_four_b, p->d_proj,
                     p->d_xcoef, p->d_chk, p->d_chk_off, p->d_fft_roots, p->d_fft_ptw, p->d_fft_iptw, p->d_ptab2, p->d_chunk_m, p->d_xtile};
     for (void* q : ptrs)
@@ -227,6 +227,11 @@ static void plan_build(pswe_plan* p, int R, int nlat, int nlon, int mode) {
     p->d_seed = upload(seed);
     p->d_rec = upload(rec);
     p->d_eps = upload(eps);
+    {
+        std::vector<double> rl(p->R + 2, 0.0);
+        for (int s = 1; s <= p->R + 1; ++s) rl[s] = 1.0 / ((double)s * (s + 1.0));
+        p->d_rlap = upload(rl);
+    }
     p->d_rowc = upload(p->cosphi);
     p->d_roww = upload(p->w);
     p->d_rowmu = upload(p->mu);

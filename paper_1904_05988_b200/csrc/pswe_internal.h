@@ -86,6 +86,7 @@ struct pswe_plan {
     double* d_seed = nullptr;    // [(R+1) * J] P^m_m(mu_j) (legendre.cpp:26-29)
     double2* d_rec = nullptr;    // [Kx] (1/eps(m,s+1), eps(m,s)/eps(m,s+1)) at off_ext(m)+s-m
     double* d_eps = nullptr;     // [Kx] eps(m, s) at off_ext(m)+s-m, s = m..R+1
+    double* d_rlap = nullptr;    // [R+2] 1/(s(s+1)), s >= 1 (inverse Laplacian factor)
     double* d_ptab = nullptr;    // STREAM mode: [Kx * J] P^m_s(mu_j), block m: [j][s]
     double2* d_chk = nullptr;    // [sum_m ceil((R+2-m)/16)][J] (P_t, P_{t-1}) at t = 16c (forward DMMA)
     int* d_chk_off = nullptr;    // [R+2] chunk offsets per m into d_chk
