@@ -26,8 +26,13 @@ void eval_imex(pswe_plan& P, const pswe_params& prm, const double2* state, doubl
                int n, cudaStream_t st) {
     P.reserve(n);
     legendre_inverse(P, INV_EVAL, state, nullptr, n, prm.radius, P.d_four_a, st);
-    fft_eval_products(P, prm, P.d_four_a, P.d_four_b, n, st);
-    legendre_forward(P, P.d_four_b, 5, n, P.d_proj, true, st);
+    if (gt_path_ok(P, n)) {  // grid stage writes forward G tiles directly
+        fft_eval_products_gt(P, prm, P.d_four_a, n, st);
+        legendre_forward_gt(P, n, P.d_proj, st);
+    } else {
+        fft_eval_products(P, prm, P.d_four_a, P.d_four_b, n, st);
+        legendre_forward(P, P.d_four_b, 5, n, P.d_proj, true, st);
+    }
     eval_tail(P, prm, P.d_proj, state, f_imp, f_exp, n, st);
 }
 
@@ -173,9 +178,12 @@ int pswe_eval_imex_timed(pswe_plan* P, const pswe_params* p, const double* state
         PSWE_CUDA(cudaEventRecord(ev[0], st));
         legendre_inverse(*P, INV_EVAL, c2(state), nullptr, n, p->radius, P->d_four_a, st);
         PSWE_CUDA(cudaEventRecord(ev[1], st));
-        fft_eval_products(*P, *p, P->d_four_a, P->d_four_b, n, st);
+        const bool gt = gt_path_ok(*P, n);
+        if (gt) fft_eval_products_gt(*P, *p, P->d_four_a, n, st);
+        else fft_eval_products(*P, *p, P->d_four_a, P->d_four_b, n, st);
         PSWE_CUDA(cudaEventRecord(ev[2], st));
-        legendre_forward(*P, P->d_four_b, 5, n, P->d_proj, true, st);
+        if (gt) legendre_forward_gt(*P, n, P->d_proj, st);
+        else legendre_forward(*P, P->d_four_b, 5, n, P->d_proj, true, st);
         PSWE_CUDA(cudaEventRecord(ev[3], st));
         eval_tail(*P, *p, P->d_proj, c2(state), c2(f_imp), c2(f_exp), n, st);
         PSWE_CUDA(cudaEventRecord(ev[4], st));

@@ -167,12 +167,15 @@ __device__ __forceinline__ double2 c2r_z(double2 a, double2 bb, double2 w) {
     return make_double2(e.x - o.y, e.y + o.x);
 }
 
-template <int N>
+// GT: write the products as forward-Legendre G tiles (GtLayout, pswe_internal.h) instead of
+// Fourier rows [q][m][i]: for each m the block's 5 fields are one 80-byte run.
+template <int N, bool GT>
 __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
     fft_eval_ip_kernel(int R, int nlat, const double2* __restrict__ TW, const double2* __restrict__ post,
                        const double2* __restrict__ four_in, double2* __restrict__ four_out,
                        const double* __restrict__ rowc, const double* __restrict__ roww,
-                       const double* __restrict__ rowmu, double phi_bar, double omega, double inv_a) {
+                       const double* __restrict__ rowmu, double phi_bar, double omega, double inv_a,
+                       GtLayout gl) {
     extern __shared__ double2 A[];  // [5][N], ipad layout; then the twiddles [ip_ntw(N)]
     double2* sTW = A + 5 * ipadded(N);
     const int i = blockIdx.x, b = blockIdx.y;
@@ -246,6 +249,19 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
     const double sflux = (1.0 / nl) * (inv_a * roww[i] / (c * c));
     const double ske = (1.0 / nl) * roww[i];
     double2* out = four_out + (long)b * 5 * rowsz + i;
+    double2* gt = nullptr;
+    long gstep = 0;
+    bool equator = false;
+    if constexpr (GT) {
+        const int J = (nlat + 1) / 2;
+        const bool north = i >= nlat - J;
+        const int j = north ? i - (nlat - J) : J - 1 - i;
+        const int z = b / gl.spg, bl = b - z * gl.spg;
+        equator = north && (J - 1 - j == i);  // odd nlat: the equator row is its own mirror
+        const long row = (((long)z * (R + 1) * gl.ns8 + (j >> 3)) * 2 + (north ? 0 : 1)) * 8 + (j & 7);
+        gt = reinterpret_cast<double2*>(reinterpret_cast<double*>(four_out) + row * gl.sgc + 10 * bl);
+        gstep = (long)gl.ns8 * 2 * 8 * gl.sgc / 2;  // double2 stride between consecutive m
+    }
     for (int k = threadIdx.x; k <= R; k += kIpThreads) {
         const double2 w = __ldg(post + k);
 #pragma unroll
@@ -257,15 +273,21 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
             const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);
             const double2 x = cadd(e, cmul(w, o));
             const double sc = q < 4 ? sflux : ske;
-            out[q * rowsz + (long)k * nlat] = make_double2(x.x * sc, x.y * sc);
+            if constexpr (GT) {
+                gt[k * gstep + q] = make_double2(x.x * sc, x.y * sc);
+                if (equator) gt[k * gstep + q + 8 * gl.sgc / 2] = make_double2(0.0, 0.0);  // G_S := 0
+            } else {
+                out[q * rowsz + (long)k * nlat] = make_double2(x.x * sc, x.y * sc);
+            }
         }
     }
 }
 
-template <int N>
-bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n, cudaStream_t st) {
+template <int N, bool GT = false>
+bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n, cudaStream_t st,
+             GtLayout gl = GtLayout()) {
     const size_t sm = (size_t)(5 * ipadded(N) + ip_ntw(N)) * sizeof(double2);
-    auto kern = fft_eval_ip_kernel<N>;
+    auto kern = fft_eval_ip_kernel<N, GT>;
     static bool attr = false;  // once per instantiation
     if (!attr) {
         if (sm > 48 * 1024)
@@ -276,7 +298,7 @@ bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, dou
         attr = true;
     }
     kern<<<dim3(P.nlat, n), kIpThreads, sm, st>>>(P.R, P.nlat, P.d_fft_iptw, P.d_fft_post, fin, fout, P.d_rowc,
-                                                  P.d_roww, P.d_rowmu, prm.phi_bar, prm.omega, 1.0 / prm.radius);
+                                                  P.d_roww, P.d_rowmu, prm.phi_bar, prm.omega, 1.0 / prm.radius, gl);
     PSWE_LAUNCH_CHECK();
     return true;
 }
@@ -310,6 +332,26 @@ bool fft_eval_products_ip(const pswe_plan& P, const pswe_params& prm, const doub
         PSWE_CASE(256) PSWE_CASE(384) PSWE_CASE(512) PSWE_CASE(768) PSWE_CASE(1024) PSWE_CASE(1536)
 #undef PSWE_CASE
         default: return false;
+    }
+}
+
+bool gt_path_ok(const pswe_plan& P, int n) {
+    static const bool off = [] { const char* e = getenv("PSWE_FFT_STOCKHAM"); return e && atoi(e) != 0; }();
+    static const bool gt_off = [] { const char* e = getenv("PSWE_NO_GTILE"); return e && atoi(e) != 0; }();
+    return !off && !gt_off && P.legendre_mode == PSWE_LEGENDRE_STREAM && !P.simt && P.n_chunks > 0 &&
+           ip_radix(P.N, 0) != 0 && P.d_gtile != nullptr && gt_layout(P.R, P.J, n).doubles <= P.gtile_cap;
+}
+
+void fft_eval_products_gt(const pswe_plan& P, const pswe_params& prm, const double2* fin, int n, cudaStream_t st) {
+    const GtLayout gl = gt_layout(P.R, P.J, n);
+    double2* g = reinterpret_cast<double2*>(P.d_gtile);
+    switch (P.N) {
+#define PSWE_CASE(NN) \
+    case NN: eval_ip<NN, true>(P, prm, fin, g, n, st, gl); return;
+        PSWE_CASE(24) PSWE_CASE(32) PSWE_CASE(48) PSWE_CASE(64) PSWE_CASE(96) PSWE_CASE(128) PSWE_CASE(192)
+        PSWE_CASE(256) PSWE_CASE(384) PSWE_CASE(512) PSWE_CASE(768) PSWE_CASE(1024) PSWE_CASE(1536)
+#undef PSWE_CASE
+        default: throw std::logic_error("fft_eval_products_gt: no in-place plan for this grid");
     }
 }
 

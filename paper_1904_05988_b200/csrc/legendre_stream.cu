@@ -152,8 +152,10 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
         load_tile(tiles, pm + (long)warp * Jp * 16, lane);
         cp_async_commit();
     }
+#ifndef PSWE_FDIAG_NOSTAGE
     legc::stage_g<NT, 8>(G, Jp * SG, Jp, J, nlat, R, m, q0, nq, four,
                          [](int j, int col) { return gpos<NT>(j, col); });
+#endif
     __syncthreads();
     const int r4 = lane >> 2, c4 = lane & 3;
     bool first = true;
@@ -165,13 +167,17 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
 #pragma unroll
             for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
         const double* src = pm + (long)c * Jp * 16;
+#ifndef PSWE_FDIAG_NOTILE
         if (!first) {  // the first task's tile was issued before the G staging
             load_tile(tiles, src, lane);
             cp_async_commit();
         }
+#endif
         first = false;
         for (int sl = 0; sl < nsl; ++sl) {
+#ifndef PSWE_FDIAG_NOTILE
             if (sl + 1 < nsl) load_tile(tiles + ((sl + 1) & 1) * 32 * 16, src + (long)(sl + 1) * 32 * 16, lane);
+#endif
             cp_async_commit();
             cp_async_wait<1>();
             __syncwarp();
@@ -185,7 +191,11 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) {
                         const double af = G[par * Jp * SG + gpos<NT>(jk, 8 * nt + r4)];  // A[m=col][k=lat]
+#ifdef PSWE_FDIAG_NODMMA
+                        acc[par][nt][0] += af * bf;
+#else
                         dmma(acc[par][nt], af, bf);
+#endif
                     }
                 }
             }
@@ -210,6 +220,151 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
                 }
         }
     }
+}
+
+// ---- forward on G tiles -------------------------------------------------------------------
+// Task (m, chunk group g) of the plan's task list (longest first), column group z = blockIdx.y.
+// W warps x CPW chunks: warp w owns chunks 8g + CPW w + {0..CPW-1} (2 CPW n-tiles: even/odd
+// degrees) for all NTC column tiles. K (latitude) streams in 8-latitude stages: one bulk copy of
+// the G tile (both hemispheres, written in this layout by the grid stage) and one 1 KB copy per
+// chunk of the P table, into an S-stage mbarrier ring. G_E = G_N + G_S and G_O = G_N - G_S are
+// formed in registers from the two hemisphere fragments, so per k-step a warp issues 2 NTC +
+// 2 CPW fragment loads for 2 NTC CPW DMMAs.
+template <int NTC, int W, int CPW, int S>
+__global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int nq, GtLayout gl,
+                                                           const double* __restrict__ ptab,
+                                                           const int* __restrict__ cbase,
+                                                           const int2* __restrict__ tasks,
+                                                           const double* __restrict__ gt,
+                                                           double2* __restrict__ out) {
+    constexpr int NCH = W * CPW;
+    extern __shared__ __align__(128) double smem[];
+    const int sgc = gl.sgc;
+    const int gstage = 2 * 8 * sgc;              // doubles of one G stage
+    double* sG = smem;                           // [S][2][8][sgc]
+    double* sP = sG + S * gstage;                // [S][NCH][8 * 16]
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(sP + S * NCH * 128);
+    unsigned long long* empty = full + S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int2 tk = tasks[blockIdx.x];
+    const int m = tk.x;
+    const int z = blockIdx.y;
+    const int len = R + 2 - m;
+    const int nch = (len + CH - 1) / CH;
+    const int c0 = tk.y * NCH;
+    const int nval = min(NCH, nch - c0);
+    const int ns8 = gl.ns8;
+    const double* __restrict__ pm = ptab + (long)(cbase[m] + c0) * Jp * 16;
+    const double* __restrict__ gm = gt + ((long)z * (R + 1) + m) * ns8 * gstage;
+    const int r4 = lane >> 2, c4 = lane & 3;
+    const unsigned GB = (unsigned)gstage * sizeof(double);
+
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < S; ++k) {
+            mbar_init(full + k, 1);
+            mbar_init(empty + k, W);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int s8) {
+        const int k = s8 % S;
+        mbar_expect_tx(full + k, GB + nval * 1024u);
+        bulk_g2s(sG + k * gstage, gm + (long)s8 * gstage, GB, full + k);
+        const double* ps = pm + (s8 >> 2) * 512 + (s8 & 3) * 128;
+        for (int u = 0; u < nval; ++u) bulk_g2s(sP + (k * NCH + u) * 128, ps + (long)u * Jp * 16, 1024u, full + k);
+    };
+    if (threadIdx.x == 0)
+        for (int s8 = 0; s8 < S && s8 < ns8; ++s8) issue(s8);
+
+    double acc[NTC][CPW][2][2];
+#pragma unroll
+    for (int a = 0; a < NTC; ++a)
+#pragma unroll
+        for (int b = 0; b < CPW; ++b) acc[a][b][0][0] = acc[a][b][0][1] = acc[a][b][1][0] = acc[a][b][1][1] = 0.0;
+    const bool active = warp * CPW < nval;
+
+    for (int s8 = 0; s8 < ns8; ++s8) {
+        const int k = s8 % S;
+        const unsigned ph = (unsigned)(s8 / S) & 1u;
+        mbar_wait(full + k, ph);
+        __syncwarp();
+        if (active) {
+            const double* g = sG + k * gstage;
+            const double* pt = sP + (k * NCH + warp * CPW) * 128;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const int rr = 4 * ks + c4;  // latitude row of this lane's k
+                double ae[NTC], ao[NTC], bf[CPW][2];
+#pragma unroll
+                for (int nt = 0; nt < NTC; ++nt) {
+                    const double gn = g[rr * sgc + 8 * nt + r4];
+                    const double gs = g[(8 + rr) * sgc + 8 * nt + r4];
+                    ae[nt] = gn + gs;
+                    ao[nt] = gn - gs;
+                }
+#pragma unroll
+                for (int cc = 0; cc < CPW; ++cc)
+#pragma unroll
+                    for (int par = 0; par < 2; ++par) bf[cc][par] = pt[cc * 128 + rr * 16 + pswz(c4, par * 8 + r4)];
+#pragma unroll
+                for (int nt = 0; nt < NTC; ++nt)
+#pragma unroll
+                    for (int cc = 0; cc < CPW; ++cc) {
+                        dmma(acc[nt][cc][0], ae[nt], bf[cc][0]);
+                        dmma(acc[nt][cc][1], ao[nt], bf[cc][1]);
+                    }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + k);
+        if (threadIdx.x == 0 && s8 + S < ns8) {
+            mbar_wait(empty + k, ph);
+            issue(s8 + S);
+        }
+    }
+    if (!active) return;
+    // C[m = column 8 nt + r4][n = degree-in-parity 2 c4 + v]: t = 16 c + par + 2 (2 c4 + v)
+    const long Kx = (long)(R + 1) * (R + 4) / 2;
+    const long bx = off_ext(R, m);
+    const int qz = z * 5 * gl.spg;
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt) {
+        const int col = 8 * nt + r4;
+        const int q = qz + (col >> 1);
+        if ((col >> 1) >= 5 * gl.spg || q >= nq) continue;
+#pragma unroll
+        for (int cc = 0; cc < CPW; ++cc) {
+            const int c = c0 + warp * CPW + cc;
+            if (c >= nch) continue;
+#pragma unroll
+            for (int par = 0; par < 2; ++par)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int t = c * CH + par + 2 * (2 * c4 + v);
+                    if (t >= len) continue;
+                    reinterpret_cast<double*>(out + (long)q * Kx + bx + t)[col & 1] = acc[nt][cc][par][v];
+                }
+        }
+    }
+}
+
+template <int NTC>
+void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out, cudaStream_t st) {
+    constexpr int W = 4, CPW = 2, S = 4;
+    static_assert(W * CPW == kFwdChunksPerTask, "task table granularity");
+    const int Jp = ((P.J + 31) / 32) * 32;
+    const size_t sm = (size_t)S * (2 * 8 * gl.sgc + W * CPW * 128) * sizeof(double) +
+                      2 * S * sizeof(unsigned long long);
+    auto kern = leg_fwd_gt_kernel<NTC, W, CPW, S>;
+    static int attr = 0;
+    if ((int)sm > attr) {
+        PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr = (int)sm;
+    }
+    kern<<<dim3(P.n_fwd_tasks, gl.groups), 32 * W, sm, st>>>(P.R, Jp, nq, gl, P.d_ptab2, P.d_chk_off,
+                                                             P.d_fwd_tasks, P.d_gtile, out);
+    PSWE_LAUNCH_CHECK();
 }
 
 // ---- inverse ------------------------------------------------------------------------------
@@ -477,6 +632,20 @@ void inv_tma_launch(const pswe_plan& P, const double* Xt, int nq, double2* out, 
 
 }  // namespace
 
+// Forward Legendre of the eval grid stage's 5 projections of n states from the G tiles (ext
+// layout out[5n][Kx]); preconditions: gt_path_ok(P, n).
+void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t st) {
+    const GtLayout gl = gt_layout(P.R, P.J, n);
+    switch (gl.ntc) {
+        case 2: fwd_gt_launch<2>(P, gl, 5 * n, out, st); break;
+        case 3: fwd_gt_launch<3>(P, gl, 5 * n, out, st); break;
+        case 4: fwd_gt_launch<4>(P, gl, 5 * n, out, st); break;
+        case 5: fwd_gt_launch<5>(P, gl, 5 * n, out, st); break;
+        case 7: fwd_gt_launch<7>(P, gl, 5 * n, out, st); break;
+        default: throw std::logic_error("legendre_forward_gt: unexpected column tiling");
+    }
+}
+
 // Streamed P table (STREAM mode), built at plan creation; layout in the file header.
 void build_legendre_table2(pswe_plan& P) {
     const int Jp = ((P.J + 31) / 32) * 32;
@@ -491,6 +660,13 @@ void build_legendre_table2(pswe_plan& P) {
         for (int c = off[m]; c < off[m + 1]; ++c) cm[c] = m;
     PSWE_CUDA(cudaMalloc(&P.d_chunk_m, cm.size() * sizeof(int)));
     PSWE_CUDA(cudaMemcpy(P.d_chunk_m, cm.data(), cm.size() * sizeof(int), cudaMemcpyHostToDevice));
+    // forward tasks (m, group of kFwdChunksPerTask chunks), longest (small m) first
+    std::vector<int2> tasks;
+    for (int m = 0; m <= P.R; ++m)
+        for (int g = 0; g * kFwdChunksPerTask < off[m + 1] - off[m]; ++g) tasks.push_back(make_int2(m, g));
+    P.n_fwd_tasks = (int)tasks.size();
+    PSWE_CUDA(cudaMalloc(&P.d_fwd_tasks, tasks.size() * sizeof(int2)));
+    PSWE_CUDA(cudaMemcpy(P.d_fwd_tasks, tasks.data(), tasks.size() * sizeof(int2), cudaMemcpyHostToDevice));
     dim3 grid((Jp + 127) / 128, P.R + 1);
     build_ptab2_kernel<<<grid, 128>>>(P.R, P.J, Jp, P.d_mu_n, P.d_seed, P.d_rec, P.d_chk_off, P.d_ptab2);
     PSWE_LAUNCH_CHECK();

@@ -95,6 +95,10 @@ struct pswe_plan {
     int* d_chunk_m = nullptr;    // STREAM mode: [n_chunks] order m of each chunk
     mutable double* d_xtile = nullptr;  // STREAM mode: inverse X tiles (grow-only scratch)
     mutable size_t xtile_cap = 0;       // doubles
+    int2* d_fwd_tasks = nullptr;  // STREAM mode: forward (m, chunk group) tasks, longest first
+    int n_fwd_tasks = 0;
+    double* d_gtile = nullptr;    // STREAM mode: grid-stage products as forward G tiles (GtLayout)
+    size_t gtile_cap = 0;         // doubles
     double* d_rowc = nullptr;    // [nlat] cos(phi_i)
     double* d_roww = nullptr;    // [nlat] Gauss weight w_i
     double* d_rowmu = nullptr;   // [nlat] mu_i
@@ -114,6 +118,27 @@ struct pswe_plan {
 };
 
 namespace pswe {
+
+// Forward-Legendre G tiles written by the fused grid stage (fft_ip.cu) and read by bulk copies in
+// legendre_stream.cu: per column group z (spg states = 10 spg real columns), order m, 8-latitude
+// slice s, hemisphere h (0 = north row nlat-J+j, 1 = south row J-1-j), latitude row r:
+//   gt[((((z (R+1) + m) ns8 + s) 2 + h) 8 + r) sgc + 10 b' + 2 f + {re, im}]
+// for state b = spg z + b', field f of (Phi'U, Phi'V, qU, qV, ke); sgc = 4 mod 16 doubles.
+struct GtLayout {
+    int spg = 0, groups = 0, ntc = 0, sgc = 0, ns8 = 0;
+    size_t doubles = 0;
+};
+constexpr int kFwdChunksPerTask = 8;  // forward task = (m, 8 chunks): 4 warps x 2 chunks
+inline GtLayout gt_layout(int R, int J, int n) {
+    GtLayout g;
+    g.spg = n < 5 ? n : 5;
+    g.groups = (n + g.spg - 1) / g.spg;
+    g.ntc = (10 * g.spg + 7) / 8;
+    g.sgc = 8 * g.ntc + ((8 * g.ntc) % 16 == 0 ? 4 : 12);
+    g.ns8 = ((J + 31) / 32) * 4;
+    g.doubles = (size_t)g.groups * (R + 1) * g.ns8 * 2 * 8 * g.sgc;
+    return g;
+}
 
 // legendre.cu
 enum InvKind { INV_PLAIN = 0, INV_UV = 1, INV_EVAL = 2 };
@@ -156,6 +181,11 @@ void fft_eval_products(const pswe_plan& P, const pswe_params& prm, const double2
 
 // fft2.cu: compile-time-sized variants; return false if nlon/2 is not instantiated
 std::vector<double2> fft_pass_twiddles(int N);
+// G-tile path of the eval grid stage (STREAM mode): fft_ip.cu writes P.d_gtile, the forward
+// reads it (legendre_stream.cu). gt_path_ok: every precondition of the pair holds for n states.
+bool gt_path_ok(const pswe_plan& P, int n);
+void fft_eval_products_gt(const pswe_plan& P, const pswe_params& prm, const double2* fin, int n, cudaStream_t st);
+void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t st);
 // fft_ip.cu: in-place fused grid stage; false if nlon/2 has no in-place plan
 std::vector<double2> fft_ip_twiddles(int N);
 bool fft_eval_products_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
