@@ -249,8 +249,9 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
     const double sflux = (1.0 / nl) * (inv_a * roww[i] / (c * c));
     const double ske = (1.0 / nl) * roww[i];
     double2* out = four_out + (long)b * 5 * rowsz + i;
-    double2* gt = nullptr;
+    double* gt = nullptr;
     long gstep = 0;
+    int swz = 0, gcol = 0;
     bool equator = false;
     if constexpr (GT) {
         const int J = (nlat + 1) / 2;
@@ -259,8 +260,10 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
         const int z = b / gl.spg, bl = b - z * gl.spg;
         equator = north && (J - 1 - j == i);  // odd nlat: the equator row is its own mirror
         const long row = (((long)z * (R + 1) * gl.ns8 + (j >> 3)) * 2 + (north ? 0 : 1)) * 8 + (j & 7);
-        gt = reinterpret_cast<double2*>(reinterpret_cast<double*>(four_out) + row * gl.sgc + 10 * bl);
-        gstep = (long)gl.ns8 * 2 * 8 * gl.sgc / 2;  // double2 stride between consecutive m
+        gt = reinterpret_cast<double*>(four_out) + row * gl.sgc;
+        gstep = (long)gl.ns8 * 2 * 8 * gl.sgc;  // doubles between consecutive m
+        swz = gt_swz(gl.ntc, j & 7);
+        gcol = 10 * bl;
     }
     for (int k = threadIdx.x; k <= R; k += kIpThreads) {
         const double2 w = __ldg(post + k);
@@ -274,8 +277,9 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
             const double2 x = cadd(e, cmul(w, o));
             const double sc = q < 4 ? sflux : ske;
             if constexpr (GT) {
-                gt[k * gstep + q] = make_double2(x.x * sc, x.y * sc);
-                if (equator) gt[k * gstep + q + 8 * gl.sgc / 2] = make_double2(0.0, 0.0);  // G_S := 0
+                double* d = gt + k * gstep + ((gcol + 2 * q) ^ swz);
+                *reinterpret_cast<double2*>(d) = make_double2(x.x * sc, x.y * sc);
+                if (equator) *reinterpret_cast<double2*>(d + 8 * gl.sgc) = make_double2(0.0, 0.0);  // G_S := 0
             } else {
                 out[q * rowsz + (long)k * nlat] = make_double2(x.x * sc, x.y * sc);
             }

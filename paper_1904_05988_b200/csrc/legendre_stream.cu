@@ -269,13 +269,25 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
     __syncthreads();
     auto issue = [&](int s8) {
         const int k = s8 % S;
+#if defined(PSWE_GDIAG_NOG)
+        mbar_expect_tx(full + k, nval * 1024u);
+#elif defined(PSWE_GDIAG_NOP)
+        mbar_expect_tx(full + k, GB);
+#else
         mbar_expect_tx(full + k, GB + nval * 1024u);
+#endif
+#ifndef PSWE_GDIAG_NOG
         bulk_g2s(sG + k * gstage, gm + (long)s8 * gstage, GB, full + k);
+#endif
+#ifndef PSWE_GDIAG_NOP
         const double* ps = pm + (s8 >> 2) * 512 + (s8 & 3) * 128;
         for (int u = 0; u < nval; ++u) bulk_g2s(sP + (k * NCH + u) * 128, ps + (long)u * Jp * 16, 1024u, full + k);
+#endif
     };
+#ifndef PSWE_GDIAG_NOTMA
     if (threadIdx.x == 0)
         for (int s8 = 0; s8 < S && s8 < ns8; ++s8) issue(s8);
+#endif
 
     double acc[NTC][CPW][2][2];
 #pragma unroll
@@ -287,7 +299,9 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
     for (int s8 = 0; s8 < ns8; ++s8) {
         const int k = s8 % S;
         const unsigned ph = (unsigned)(s8 / S) & 1u;
+#ifndef PSWE_GDIAG_NOTMA
         mbar_wait(full + k, ph);
+#endif
         __syncwarp();
         if (active) {
             const double* g = sG + k * gstage;
@@ -298,8 +312,9 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
                 double ae[NTC], ao[NTC], bf[CPW][2];
 #pragma unroll
                 for (int nt = 0; nt < NTC; ++nt) {
-                    const double gn = g[rr * sgc + 8 * nt + r4];
-                    const double gs = g[(8 + rr) * sgc + 8 * nt + r4];
+                    const int cs = (8 * nt + r4) ^ gt_swz(NTC, rr);
+                    const double gn = g[rr * sgc + cs];
+                    const double gs = g[(8 + rr) * sgc + cs];
                     ae[nt] = gn + gs;
                     ao[nt] = gn - gs;
                 }
@@ -317,11 +332,13 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
             }
         }
         __syncwarp();
+#ifndef PSWE_GDIAG_NOTMA
         if (lane == 0) mbar_arrive(empty + k);
         if (threadIdx.x == 0 && s8 + S < ns8) {
             mbar_wait(empty + k, ph);
             issue(s8 + S);
         }
+#endif
     }
     if (!active) return;
     // C[m = column 8 nt + r4][n = degree-in-parity 2 c4 + v]: t = 16 c + par + 2 (2 c4 + v)

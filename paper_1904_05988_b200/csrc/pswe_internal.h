@@ -123,18 +123,22 @@ namespace pswe {
 // legendre_stream.cu: per column group z (spg states = 10 spg real columns), order m, 8-latitude
 // slice s, hemisphere h (0 = north row nlat-J+j, 1 = south row J-1-j), latitude row r:
 //   gt[((((z (R+1) + m) ns8 + s) 2 + h) 8 + r) sgc + 10 b' + 2 f + {re, im}]
-// for state b = spg z + b', field f of (Phi'U, Phi'V, qU, qV, ke); sgc = 4 mod 16 doubles.
+// for state b = spg z + b', field f of (Phi'U, Phi'V, qU, qV, ke), the column XOR-swizzled per
+// row by gt_swz (sgc = 8 ntc doubles, no padding; the forward's fragment reads are then
+// conflict-free).
 struct GtLayout {
     int spg = 0, groups = 0, ntc = 0, sgc = 0, ns8 = 0;
     size_t doubles = 0;
 };
 constexpr int kFwdChunksPerTask = 8;  // forward task = (m, 8 chunks): 4 warps x 2 chunks
+// column swizzle of latitude row r (0..7) of a G tile with ntc 8-column tiles
+__host__ __device__ inline int gt_swz(int ntc, int r) { return (ntc & 1) ? 4 * ((r >> 1) & 1) : 4 * (r & 3); }
 inline GtLayout gt_layout(int R, int J, int n) {
     GtLayout g;
     g.spg = n < 5 ? n : 5;
     g.groups = (n + g.spg - 1) / g.spg;
     g.ntc = (10 * g.spg + 7) / 8;
-    g.sgc = 8 * g.ntc + ((8 * g.ntc) % 16 == 0 ? 4 : 12);
+    g.sgc = 8 * g.ntc;
     g.ns8 = ((J + 31) / 32) * 4;
     g.doubles = (size_t)g.groups * (R + 1) * g.ns8 * 2 * 8 * g.sgc;
     return g;
