@@ -10,8 +10,10 @@ Headline metric (BASELINE.json): SWE RHS evals/s (fp64 SH fwd+inv) at T255.
 Side results on the same JSON line:
   e2e            same metric through the public API with pinned HOST buffers, H2D + D2H inside
                  the timed region;
-  roofline       dominant kernel's algorithmic FP64 flops / its event-timed duration vs the
-                 FP64 peak measured in-run (MEASURED_PEAKS.json has no FP64 figure);
+  roofline       dominant (longest) stage's algorithmic work / its event-timed duration: FP64
+                 flops vs the FP64 DMMA peak measured in-run for the Legendre stages (MEASURED_
+                 PEAKS.json has no FP64 figure), bytes vs MEASURED_PEAKS.json hbm_gbs for the
+                 grid stage and the tail; every stage is listed under roofline.stages;
   cpu_baseline   the reference (oracle/_ref, compiled from /root/reference) timed on the host
                  cores, rank 0 at N=1 only;
   pfasst         config-3-shape PFASST block (T255/T127, 5/3 nodes, dt 60 s, 8 steps, 4 its),
@@ -256,30 +258,54 @@ def run_ours(args):
                                           fe.data_ptr(), BATCH, _stream(), ms4))
         stage += np.array(list(ms4))
     stage /= args.steps
-    J = NLAT // 2
     F_L = NLAT * (R_BENCH + 1) * (R_BENCH + 2)  # flops per complex field per direction
-    nlog = math.log2(NLON)
-    fft_flops = 2.5 * NLAT * NLON * nlog  # per real row-field per direction
-    algo = {
-        "legendre_inverse": 4 * BATCH * F_L,            # Phi, zeta, U, V
-        "fft_products": 9 * BATCH * fft_flops + 15.0 * BATCH * NLAT * NLON,
-        "legendre_forward": 5 * BATCH * F_L,            # Phi'U, Phi'V, qU, qV, ke
-        "tail": 30.0 * BATCH * P.num_coeffs(R_BENCH),
+    rowb = (R_BENCH + 1) * NLAT * 16               # bytes of one field's Fourier rows (m <= R)
+    Kb = P.num_coeffs(R_BENCH) * 16                # bytes of one spectral field
+    # per-stage algorithmic work: the Legendre stages are FP64-tensor
+    # bound (flops), the grid stage and the tail stream bytes (HBM)
+    work = {
+        "legendre_inverse": ("tensor", 4 * BATCH * F_L),           # Phi, zeta, U, V
+        "fft_products": ("hbm", (4 + 5) * BATCH * rowb),            # 4 fields in, 5 products out
+        "legendre_forward": ("tensor", 5 * BATCH * F_L),           # Phi'U, Phi'V, qU, qV, ke
+        "tail": ("hbm", BATCH * (5 + 3 + 6) * Kb),                 # 5 projections + state in, 2 x 3 out
     }
-    names = list(algo)
-    dom = names[int(np.argmax(stage))]
+    names = list(work)
     peak_dfma = float(L.pswe_fp64_peak(0, 4096))
     peak_dmma = float(L.pswe_fp64_peak(1, 2048))
-    achieved = algo[dom] / (stage[names.index(dom)] * 1e-3) / 1e12
-    peak = max(peak_dfma, peak_dmma)
+    peak_fp64 = max(peak_dfma, peak_dmma)
+    peak = peak_fp64
+    hbm_peak, hbm_src = 6650.0, "of fallback (B200_PROFILING.md: 6.65 TB/s)"
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm_peak, hbm_src = float(mp["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+    except Exception:
+        pass
+    try:  # per-launch DRAM traffic of each stage's kernels from the committed ncu --set full capture
+        traffic_tab = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["stages"]
+    except Exception:
+        traffic_tab = {}
+    stages = {}
+    for n, v in zip(names, stage):
+        kind, amount = work[n]
+        sec = v * 1e-3
+        if kind == "tensor":
+            ach, pk, unit = amount / sec / 1e12, peak_fp64, "TFLOP/s"
+        else:
+            ach, pk, unit = amount / sec / 1e9, hbm_peak, "GB/s"
+        stages[n] = {"bound": kind, "ms": float(v), "achieved": ach, "peak": pk, "unit": unit, "frac": ach / pk,
+                     "algorithmic": amount, "traffic": traffic_tab.get(n)}
+    dom = names[int(np.argmax(stage))]
+    d = stages[dom]
     roofline = {
-        "bound": "tensor", "pipe": "fp64", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": achieved / peak, "traffic": None,
-        "peak_source": f"measured in-run FP64 microbenchmarks (DFMA {peak_dfma:.1f}, DMMA m8n8k4 {peak_dmma:.1f} "
-                       f"TFLOP/s); MEASURED_PEAKS.json has no FP64 figure",
-        "algorithmic_flops_per_launch": algo[dom],
-        "stage_ms": {n: float(v) for n, v in zip(names, stage)},
-        "stage_frac_of_fp64_peak": {n: algo[n] / (v * 1e-3) / 1e12 / peak for n, v in zip(names, stage)},
+        "bound": d["bound"], "kernel": dom, "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"],
+        "frac": d["frac"], "traffic": d["traffic"],
+        "algorithmic_per_launch": d["algorithmic"],
+        "peak_source": (f"measured in-run FP64 microbenchmarks (DFMA {peak_dfma:.1f}, DMMA m8n8k4 {peak_dmma:.1f} "
+                        f"TFLOP/s; MEASURED_PEAKS.json has no FP64 figure)" if d["bound"] == "tensor"
+                        else hbm_src),
+        "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                          "ncu --set full, cache flushed)",
+        "stages": stages,
     }
 
     # e2e through the public API with pinned host buffers
