@@ -37,7 +37,7 @@ extern "C" {
 
 /* Associated-Legendre strategy ("streamed from HBM or recomputed on the fly"). */
 #define PSWE_LEGENDRE_RECOMPUTE 0 /* recurrence in registers/shared memory; no table */
-#define PSWE_LEGENDRE_STREAM 1    /* forward contraction streams a P table kept in HBM */
+#define PSWE_LEGENDRE_STREAM 1    /* both contractions stream a P table kept in HBM (bulk-copied tiles) */
 
 typedef struct pswe_plan pswe_plan;     /* TransformPlan (transform.hpp:27) on one GPU */
 typedef struct pswe_level pswe_level;   /* LevelSpec + SpaceTimeState (multilevel.hpp:16, sdc.hpp:14) */
