@@ -16,6 +16,7 @@
 // The inverse's X operand is written by its prep kernel directly as per-chunk shared-memory
 // images ([16 degrees][8 NT + 2] doubles), so each pipeline stage is W + 1 bulk copies (TMA,
 // cp.async.bulk) completing on one mbarrier; stages are released through a second mbarrier.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -222,44 +223,62 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
     }
 }
 
-// ---- forward on G tiles -------------------------------------------------------------------
-// Task (m, chunk group g) of the plan's task list (longest first), column group z = blockIdx.y.
-// W warps x CPW chunks: warp w owns chunks 8g + CPW w + {0..CPW-1} (2 CPW n-tiles: even/odd
-// degrees) for all NTC column tiles. K (latitude) streams in 8-latitude stages: one bulk copy of
-// the G tile (both hemispheres, written in this layout by the grid stage) and one 1 KB copy per
-// chunk of the P table, into an S-stage mbarrier ring. G_E = G_N + G_S and G_O = G_N - G_S are
-// formed in registers from the two hemisphere fragments, so per k-step a warp issues 2 NTC +
-// 2 CPW fragment loads for 2 NTC CPW DMMAs.
+// ---- forward on G tiles ----------------------------------------------------------------------
+// Task = a run of chunks of at most two orders m_a, m_b (plan task table, about kFwdPerSm per SM,
+// equal work); column group z = blockIdx.y. Warp w owns CPW chunks of one order (2 CPW n-tiles:
+// even and odd degrees) for all NTC column tiles. K (latitude) streams in 8-latitude stages: one
+// bulk copy of the G tile of each order (both hemispheres, written in this layout by the grid
+// stage) and one 1 KB copy per chunk of the P table, into an S-stage mbarrier ring.
+// G_E = G_N + G_S and G_O = G_N - G_S are formed in registers and reused by the CPW chunks.
 template <int NTC, int W, int CPW, int S>
 __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int nq, GtLayout gl,
                                                            const double* __restrict__ ptab,
                                                            const int* __restrict__ cbase,
-                                                           const int2* __restrict__ tasks,
+                                                           const int4* __restrict__ tasks_a,
+                                                           const int2* __restrict__ tasks_b,
                                                            const double* __restrict__ gt,
                                                            double2* __restrict__ out) {
-    constexpr int NCH = W * CPW;
+    constexpr int NS = W * CPW;  // chunk slots
     extern __shared__ __align__(128) double smem[];
+    __shared__ long pbase[NS];
+    __shared__ int pslot[NS], npc;
     const int sgc = gl.sgc;
-    const int gstage = 2 * 8 * sgc;              // doubles of one G stage
-    double* sG = smem;                           // [S][2][8][sgc]
-    double* sP = sG + S * gstage;                // [S][NCH][8 * 16]
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(sP + S * NCH * 128);
+    const int gstage = 2 * 8 * sgc;              // doubles of one order's G stage
+    double* sG = smem;                           // [S][2 orders][2][8][sgc]
+    double* sP = sG + S * 2 * gstage;            // [S][NS][8 * 16]
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(sP + S * NS * 128);
     unsigned long long* empty = full + S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int2 tk = tasks[blockIdx.x];
-    const int m = tk.x;
+    const int4 ta = tasks_a[blockIdx.x];
+    const int2 tb = tasks_b[blockIdx.x];
+    const int na = ta.z, nb = tb.y;
+    const int wa = (na + CPW - 1) / CPW;  // warps of order a
     const int z = blockIdx.y;
-    const int len = R + 2 - m;
-    const int nch = (len + CH - 1) / CH;
-    const int c0 = tk.y * NCH;
-    const int nval = min(NCH, nch - c0);
     const int ns8 = gl.ns8;
-    const double* __restrict__ pm = ptab + (long)(cbase[m] + c0) * Jp * 16;
-    const double* __restrict__ gm = gt + ((long)z * (R + 1) + m) * ns8 * gstage;
+    const bool ord_b = warp >= wa;
+    const int my_m = ord_b ? ta.w : ta.x;
+    const int my_c0 = ord_b ? tb.x + (warp - wa) * CPW : ta.y + warp * CPW;
+    const int my_n = max(0, min(CPW, ord_b ? nb - (warp - wa) * CPW : na - warp * CPW));
+    const bool mine = my_n > 0;
+    const double* __restrict__ ga = gt + ((long)z * (R + 1) + ta.x) * ns8 * gstage;
+    const double* __restrict__ gb = gt + ((long)z * (R + 1) + ta.w) * ns8 * gstage;
     const int r4 = lane >> 2, c4 = lane & 3;
     const unsigned GB = (unsigned)gstage * sizeof(double);
 
     if (threadIdx.x == 0) {
+        int n = 0;  // valid chunk slots in warp order: slot (w, u) -> table tile
+        for (int w = 0; w < W; ++w) {
+            const bool b = w >= wa;
+            const int m = b ? ta.w : ta.x;
+            const int c0 = b ? tb.x + (w - wa) * CPW : ta.y + w * CPW;
+            const int nn = max(0, min(CPW, b ? nb - (w - wa) * CPW : na - w * CPW));
+            for (int u = 0; u < nn; ++u) {
+                pbase[n] = (long)(cbase[m] + c0 + u) * Jp * 16;
+                pslot[n] = w * CPW + u;
+                ++n;
+            }
+        }
+        npc = n;
         for (int k = 0; k < S; ++k) {
             mbar_init(full + k, 1);
             mbar_init(empty + k, W);
@@ -267,49 +286,36 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
         mbar_fence_init();
     }
     __syncthreads();
+    const int np = npc;
     auto issue = [&](int s8) {
         const int k = s8 % S;
-#if defined(PSWE_GDIAG_NOG)
-        mbar_expect_tx(full + k, nval * 1024u);
-#elif defined(PSWE_GDIAG_NOP)
-        mbar_expect_tx(full + k, GB);
-#else
-        mbar_expect_tx(full + k, GB + nval * 1024u);
-#endif
-#ifndef PSWE_GDIAG_NOG
-        bulk_g2s(sG + k * gstage, gm + (long)s8 * gstage, GB, full + k);
-#endif
-#ifndef PSWE_GDIAG_NOP
-        const double* ps = pm + (s8 >> 2) * 512 + (s8 & 3) * 128;
-        for (int u = 0; u < nval; ++u) bulk_g2s(sP + (k * NCH + u) * 128, ps + (long)u * Jp * 16, 1024u, full + k);
-#endif
+        mbar_expect_tx(full + k, GB * (nb > 0 ? 2u : 1u) + np * 1024u);
+        bulk_g2s(sG + (k * 2) * gstage, ga + (long)s8 * gstage, GB, full + k);
+        if (nb > 0) bulk_g2s(sG + (k * 2 + 1) * gstage, gb + (long)s8 * gstage, GB, full + k);
+        const long ps = (s8 >> 2) * 512 + (s8 & 3) * 128;
+        for (int u = 0; u < np; ++u) bulk_g2s(sP + (k * NS + pslot[u]) * 128, ptab + pbase[u] + ps, 1024u, full + k);
     };
-#ifndef PSWE_GDIAG_NOTMA
     if (threadIdx.x == 0)
         for (int s8 = 0; s8 < S && s8 < ns8; ++s8) issue(s8);
-#endif
 
     double acc[NTC][CPW][2][2];
 #pragma unroll
     for (int a = 0; a < NTC; ++a)
 #pragma unroll
         for (int b = 0; b < CPW; ++b) acc[a][b][0][0] = acc[a][b][0][1] = acc[a][b][1][0] = acc[a][b][1][1] = 0.0;
-    const bool active = warp * CPW < nval;
 
     for (int s8 = 0; s8 < ns8; ++s8) {
         const int k = s8 % S;
         const unsigned ph = (unsigned)(s8 / S) & 1u;
-#ifndef PSWE_GDIAG_NOTMA
         mbar_wait(full + k, ph);
-#endif
         __syncwarp();
-        if (active) {
-            const double* g = sG + k * gstage;
-            const double* pt = sP + (k * NCH + warp * CPW) * 128;
+        if (mine) {
+            const double* g = sG + (k * 2 + (ord_b ? 1 : 0)) * gstage;
+            const double* pt = sP + (k * NS + warp * CPW) * 128;
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks) {
                 const int rr = 4 * ks + c4;  // latitude row of this lane's k
-                double ae[NTC], ao[NTC], bf[CPW][2];
+                double ae[NTC], ao[NTC], be[CPW], bo[CPW];
 #pragma unroll
                 for (int nt = 0; nt < NTC; ++nt) {
                     const int cs = (8 * nt + r4) ^ gt_swz(NTC, rr);
@@ -319,31 +325,31 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
                     ao[nt] = gn - gs;
                 }
 #pragma unroll
-                for (int cc = 0; cc < CPW; ++cc)
-#pragma unroll
-                    for (int par = 0; par < 2; ++par) bf[cc][par] = pt[cc * 128 + rr * 16 + pswz(c4, par * 8 + r4)];
+                for (int cc = 0; cc < CPW; ++cc) {
+                    be[cc] = pt[cc * 128 + rr * 16 + pswz(c4, r4)];
+                    bo[cc] = pt[cc * 128 + rr * 16 + pswz(c4, 8 + r4)];
+                }
 #pragma unroll
                 for (int nt = 0; nt < NTC; ++nt)
 #pragma unroll
                     for (int cc = 0; cc < CPW; ++cc) {
-                        dmma(acc[nt][cc][0], ae[nt], bf[cc][0]);
-                        dmma(acc[nt][cc][1], ao[nt], bf[cc][1]);
+                        dmma(acc[nt][cc][0], ae[nt], be[cc]);
+                        dmma(acc[nt][cc][1], ao[nt], bo[cc]);
                     }
             }
         }
         __syncwarp();
-#ifndef PSWE_GDIAG_NOTMA
         if (lane == 0) mbar_arrive(empty + k);
         if (threadIdx.x == 0 && s8 + S < ns8) {
             mbar_wait(empty + k, ph);
             issue(s8 + S);
         }
-#endif
     }
-    if (!active) return;
+    if (!mine) return;
     // C[m = column 8 nt + r4][n = degree-in-parity 2 c4 + v]: t = 16 c + par + 2 (2 c4 + v)
     const long Kx = (long)(R + 1) * (R + 4) / 2;
-    const long bx = off_ext(R, m);
+    const long bx = off_ext(R, my_m);
+    const int len = R + 2 - my_m;
     const int qz = z * 5 * gl.spg;
 #pragma unroll
     for (int nt = 0; nt < NTC; ++nt) {
@@ -352,13 +358,12 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
         if ((col >> 1) >= 5 * gl.spg || q >= nq) continue;
 #pragma unroll
         for (int cc = 0; cc < CPW; ++cc) {
-            const int c = c0 + warp * CPW + cc;
-            if (c >= nch) continue;
+            if (cc >= my_n) continue;
 #pragma unroll
             for (int par = 0; par < 2; ++par)
 #pragma unroll
                 for (int v = 0; v < 2; ++v) {
-                    const int t = c * CH + par + 2 * (2 * c4 + v);
+                    const int t = (my_c0 + cc) * CH + par + 2 * (2 * c4 + v);
                     if (t >= len) continue;
                     reinterpret_cast<double*>(out + (long)q * Kx + bx + t)[col & 1] = acc[nt][cc][par][v];
                 }
@@ -366,12 +371,10 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
     }
 }
 
-template <int NTC>
+template <int NTC, int W, int CPW, int S>
 void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out, cudaStream_t st) {
-    constexpr int W = 4, CPW = 2, S = 4;
-    static_assert(W * CPW == kFwdChunksPerTask, "task table granularity");
     const int Jp = ((P.J + 31) / 32) * 32;
-    const size_t sm = (size_t)S * (2 * 8 * gl.sgc + W * CPW * 128) * sizeof(double) +
+    const size_t sm = (size_t)S * (2 * 2 * 8 * gl.sgc + W * CPW * 128) * sizeof(double) +
                       2 * S * sizeof(unsigned long long);
     auto kern = leg_fwd_gt_kernel<NTC, W, CPW, S>;
     static int attr = 0;
@@ -379,8 +382,8 @@ void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out,
         PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr = (int)sm;
     }
-    kern<<<dim3(P.n_fwd_tasks, gl.groups), 32 * W, sm, st>>>(P.R, Jp, nq, gl, P.d_ptab2, P.d_chk_off,
-                                                             P.d_fwd_tasks, P.d_gtile, out);
+    kern<<<dim3(P.n_fwd_tasks, gl.groups), 32 * W, sm, st>>>(P.R, Jp, nq, gl, P.d_ptab2, P.d_chk_off, P.d_fwd_ta,
+                                                             P.d_fwd_tb, P.d_gtile, out);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -653,14 +656,23 @@ void inv_tma_launch(const pswe_plan& P, const double* Xt, int nq, double2* out, 
 // layout out[5n][Kx]); preconditions: gt_path_ok(P, n).
 void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t st) {
     const GtLayout gl = gt_layout(P.R, P.J, n);
-    switch (gl.ntc) {
-        case 2: fwd_gt_launch<2>(P, gl, 5 * n, out, st); break;
-        case 3: fwd_gt_launch<3>(P, gl, 5 * n, out, st); break;
-        case 4: fwd_gt_launch<4>(P, gl, 5 * n, out, st); break;
-        case 5: fwd_gt_launch<5>(P, gl, 5 * n, out, st); break;
-        case 7: fwd_gt_launch<7>(P, gl, 5 * n, out, st); break;
-        default: throw std::logic_error("legendre_forward_gt: unexpected column tiling");
+#define PSWE_FWD_CASES(W, C, S)                                                  \
+    switch (gl.ntc) {                                                            \
+        case 2: fwd_gt_launch<2, W, C, S>(P, gl, 5 * n, out, st); break;         \
+        case 3: fwd_gt_launch<3, W, C, S>(P, gl, 5 * n, out, st); break;         \
+        case 4: fwd_gt_launch<4, W, C, S>(P, gl, 5 * n, out, st); break;         \
+        case 5: fwd_gt_launch<5, W, C, S>(P, gl, 5 * n, out, st); break;         \
+        case 7: fwd_gt_launch<7, W, C, S>(P, gl, 5 * n, out, st); break;         \
+        default: throw std::logic_error("legendre_forward_gt: unexpected column tiling"); \
     }
+    static_assert(kFwdCfg[0].warps == 8 && kFwdCfg[0].cpw == 1 && kFwdCfg[0].stages == 4, "cfg 0");
+    static_assert(kFwdCfg[1].warps == 4 && kFwdCfg[1].cpw == 2 && kFwdCfg[1].stages == 3, "cfg 1");
+    if (P.fwd_cfg == 0) {
+        PSWE_FWD_CASES(8, 1, 4)
+    } else {
+        PSWE_FWD_CASES(4, 2, 3)
+    }
+#undef PSWE_FWD_CASES
 }
 
 // Streamed P table (STREAM mode), built at plan creation; layout in the file header.
@@ -677,13 +689,65 @@ void build_legendre_table2(pswe_plan& P) {
         for (int c = off[m]; c < off[m + 1]; ++c) cm[c] = m;
     PSWE_CUDA(cudaMalloc(&P.d_chunk_m, cm.size() * sizeof(int)));
     PSWE_CUDA(cudaMemcpy(P.d_chunk_m, cm.data(), cm.size() * sizeof(int), cudaMemcpyHostToDevice));
-    // forward tasks (m, group of kFwdChunksPerTask chunks), longest (small m) first
-    std::vector<int2> tasks;
-    for (int m = 0; m <= P.R; ++m)
-        for (int g = 0; g * kFwdChunksPerTask < off[m + 1] - off[m]; ++g) tasks.push_back(make_int2(m, g));
-    P.n_fwd_tasks = (int)tasks.size();
-    PSWE_CUDA(cudaMalloc(&P.d_fwd_tasks, tasks.size() * sizeof(int2)));
-    PSWE_CUDA(cudaMemcpy(P.d_fwd_tasks, tasks.data(), tasks.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    // forward tasks: all (m, chunk) in pair order m, R-m, m+1, R-m-1, ... (equal work per pair) cut
+    // into contiguous runs of at most two orders that fit kFwdWarps warps x kFwdCpw chunk slots
+    // (each order's run starts on a warp boundary), about kFwdPerSm runs per SM, so that one wave
+    // gives every SM the same work (the triangular per-m work otherwise leaves it ragged)
+    {
+        std::vector<int2> L;
+        for (int p = 0; p <= P.R - p; ++p) {
+            const int ms[2] = {p, P.R - p};
+            for (int u = 0; u < (ms[1] != ms[0] ? 2 : 1); ++u)
+                for (int c = 0; c < off[ms[u] + 1] - off[ms[u]]; ++c) L.push_back(make_int2(ms[u], c));
+        }
+        int nsm = 148;
+        {
+            int dev = 0;
+            cudaDeviceProp prop;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaGetDeviceProperties(&prop, dev) == cudaSuccess)
+                nsm = prop.multiProcessorCount;
+        }
+        P.fwd_cfg = (int)L.size() <= kFwdCfg[0].per_sm * nsm * kFwdCfg[0].warps * kFwdCfg[0].cpw ? 0 : 1;
+        const FwdCfg fc = kFwdCfg[P.fwd_cfg];
+        const int slots = fc.per_sm * nsm, cap = fc.warps * fc.cpw, cpw = fc.cpw;
+        auto used = [cpw](int na, int nb) { return (na + cpw - 1) / cpw * cpw + nb; };
+        std::vector<int4> ta;
+        std::vector<int2> tb;
+        for (int target = std::max(1, (int)((L.size() + slots - 1) / slots));; ++target) {
+            ta.clear();
+            tb.clear();
+            size_t i = 0;
+            while (i < L.size()) {
+                int4 a = make_int4(L[i].x, L[i].y, 0, -1);
+                int2 b = make_int2(0, 0);
+                int n = 0;
+                while (i < L.size() && n < std::min(target, cap)) {
+                    if (L[i].x == a.x && a.w < 0) {
+                        ++a.z;
+                    } else if ((a.w < 0 || L[i].x == a.w) && used(a.z, b.y + 1) <= cap) {
+                        if (a.w < 0) {
+                            a.w = L[i].x;
+                            b.x = L[i].y;
+                        }
+                        ++b.y;
+                    } else {
+                        break;  // a third order, or no room: new task
+                    }
+                    ++n;
+                    ++i;
+                }
+                if (a.w < 0) a.w = a.x;
+                ta.push_back(a);
+                tb.push_back(b);
+            }
+            if ((int)ta.size() <= slots || target >= cap) break;
+        }
+        P.n_fwd_tasks = (int)ta.size();
+        PSWE_CUDA(cudaMalloc(&P.d_fwd_ta, ta.size() * sizeof(int4)));
+        PSWE_CUDA(cudaMalloc(&P.d_fwd_tb, tb.size() * sizeof(int2)));
+        PSWE_CUDA(cudaMemcpy(P.d_fwd_ta, ta.data(), ta.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        PSWE_CUDA(cudaMemcpy(P.d_fwd_tb, tb.data(), tb.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
     dim3 grid((Jp + 127) / 128, P.R + 1);
     build_ptab2_kernel<<<grid, 128>>>(P.R, P.J, Jp, P.d_mu_n, P.d_seed, P.d_rec, P.d_chk_off, P.d_ptab2);
     PSWE_LAUNCH_CHECK();

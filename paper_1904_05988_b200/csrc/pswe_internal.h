@@ -95,8 +95,10 @@ struct pswe_plan {
     int* d_chunk_m = nullptr;    // STREAM mode: [n_chunks] order m of each chunk
     mutable double* d_xtile = nullptr;  // STREAM mode: inverse X tiles (grow-only scratch)
     mutable size_t xtile_cap = 0;       // doubles
-    int2* d_fwd_tasks = nullptr;  // STREAM mode: forward (m, chunk group) tasks, longest first
+    int4* d_fwd_ta = nullptr;     // STREAM mode: forward tasks (m_a, first chunk, chunks of m_a, m_b)
+    int2* d_fwd_tb = nullptr;     //   (first chunk of m_b, chunks of m_b)
     int n_fwd_tasks = 0;
+    int fwd_cfg = 0;              // index into kFwdCfg the task table was cut for
     double* d_gtile = nullptr;    // STREAM mode: grid-stage products as forward G tiles (GtLayout)
     size_t gtile_cap = 0;         // doubles
     double* d_rowc = nullptr;    // [nlat] cos(phi_i)
@@ -130,7 +132,14 @@ struct GtLayout {
     int spg = 0, groups = 0, ntc = 0, sgc = 0, ns8 = 0;
     size_t doubles = 0;
 };
-constexpr int kFwdChunksPerTask = 8;  // forward task = (m, 8 chunks): 4 warps x 2 chunks
+// forward tasks: runs of <= warps x cpw chunks of <= 2 orders m, ~per_sm runs per SM. Two
+// configurations (measured, tools/stage_times.py): one chunk per warp, 8 warps, 2 blocks/SM,
+// 4 stages when every chunk fits one wave (T255 and below); two chunks per warp (fragment reuse),
+// 4 warps, 3 blocks/SM, 3 stages otherwise.
+struct FwdCfg {
+    int warps, cpw, per_sm, stages;
+};
+constexpr FwdCfg kFwdCfg[2] = {{8, 1, 2, 4}, {4, 2, 3, 3}};
 // column swizzle of latitude row r (0..7) of a G tile with ntc 8-column tiles
 __host__ __device__ inline int gt_swz(int ntc, int r) { return (ntc & 1) ? 4 * ((r >> 1) & 1) : 4 * (r & 3); }
 inline GtLayout gt_layout(int R, int J, int n) {
