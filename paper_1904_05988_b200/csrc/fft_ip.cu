@@ -186,6 +186,8 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(TW + t));
     }
     asm volatile("cp.async.commit_group;\n" ::);
+    pdl_trigger();
+    pdl_wait();  // the Fourier rows come from the inverse Legendre kernel
     const long rowsz = (long)(R + 1) * nlat;
     const double2* in = four_in + ((long)b * 4 * nlat + i) * (R + 1);  // rows [q][i][m]
 
@@ -301,8 +303,8 @@ bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, dou
                                        (int)cudaSharedmemCarveoutMaxShared));
         attr = true;
     }
-    kern<<<dim3(P.nlat, n), kIpThreads, sm, st>>>(P.R, P.nlat, P.d_fft_iptw, P.d_fft_post, fin, fout, P.d_rowc,
-                                                  P.d_roww, P.d_rowmu, prm.phi_bar, prm.omega, 1.0 / prm.radius, gl);
+    launch_pdl(kern, dim3(P.nlat, n), dim3(kIpThreads), sm, st, P.R, P.nlat, P.d_fft_iptw, P.d_fft_post, fin, fout,
+               P.d_rowc, P.d_roww, P.d_rowmu, prm.phi_bar, prm.omega, 1.0 / prm.radius, gl);
     PSWE_LAUNCH_CHECK();
     return true;
 }

@@ -286,6 +286,8 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_trigger();
+    pdl_wait();  // G tiles come from the grid stage
     const int np = npc;
     auto issue = [&](int s8) {
         const int k = s8 % S;
@@ -382,8 +384,8 @@ void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out,
         PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr = (int)sm;
     }
-    kern<<<dim3(P.n_fwd_tasks, gl.groups), 32 * W, sm, st>>>(P.R, Jp, nq, gl, P.d_ptab2, P.d_chk_off, P.d_fwd_ta,
-                                                             P.d_fwd_tb, P.d_gtile, out);
+    launch_pdl(kern, dim3(P.n_fwd_tasks, gl.groups), dim3(32 * W), sm, st, P.R, Jp, nq, gl, P.d_ptab2, P.d_chk_off,
+               P.d_fwd_ta, P.d_fwd_tb, P.d_gtile, out);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -414,6 +416,8 @@ __global__ void xtile_prep_kernel(int R, int NQ, int SX, int nq, int nct, const 
     double2 v[PER];
 #pragma unroll
     for (int f = 0; f < PER; ++f) v[f] = make_double2(0.0, 0.0);
+    pdl_trigger();
+    pdl_wait();  // the states come from the preceding kernel
     if (bl * PER < NQ && item * PER < nq) {
         if (KIND == INV_PLAIN) {
             if (s <= R) v[0] = in[(long)item * K + bs + t];
@@ -502,6 +506,8 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
         mbar_fence_init();
     }
     __syncthreads();
+    pdl_trigger();
+    pdl_wait();  // X tiles come from the prep kernel
     auto issue = [&](int c) {
         const int k = c % S;
         mbar_expect_tx(full + k, nact * PB + XB);
@@ -645,8 +651,8 @@ void inv_tma_launch(const pswe_plan& P, const double* Xt, int nq, double2* out, 
         PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr = true;
     }
-    kern<<<dim3((nsl + WS - 1) / WS, P.R + 1, groups), 64 * WS, sm, st>>>(P.R, P.J, Jp, P.nlat, nq, P.n_chunks,
-                                                                           P.d_ptab2, P.d_chk_off, Xt, out);
+    launch_pdl(kern, dim3((nsl + WS - 1) / WS, P.R + 1, groups), dim3(64 * WS), sm, st, P.R, P.J, Jp, P.nlat, nq,
+               P.n_chunks, P.d_ptab2, P.d_chk_off, Xt, out);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -781,13 +787,13 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
     if (false)
 #endif
     if (kind == INV_EVAL)
-        xtile_prep_kernel<INV_EVAL><<<g, nthr, tsm, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
+        launch_pdl(xtile_prep_kernel<INV_EVAL>, g, dim3(nthr), tsm, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
                                                           P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     else if (kind == INV_UV)
-        xtile_prep_kernel<INV_UV><<<g, nthr, tsm, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
+        launch_pdl(xtile_prep_kernel<INV_UV>, g, dim3(nthr), tsm, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
                                                         P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     else
-        xtile_prep_kernel<INV_PLAIN><<<g, nthr, tsm, st>>>(P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
+        launch_pdl(xtile_prep_kernel<INV_PLAIN>, g, dim3(nthr), tsm, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
                                                            P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     PSWE_LAUNCH_CHECK();
 #ifdef PSWE_DIAG_NOINV

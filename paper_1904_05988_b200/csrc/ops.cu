@@ -48,6 +48,8 @@ __global__ void eval_tail_kernel(int R, const double* __restrict__ eps, const do
     const long Kx = (long)(R + 1) * (R + 4) / 2;
     const long k = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const int b = blockIdx.y;
+    pdl_trigger();
+    pdl_wait();  // the projections come from the forward Legendre kernel
     if (k >= K) return;
     int m, s;
     decode_rs(R, k, m, s);
@@ -168,7 +170,7 @@ static dim3 grid_k(int R, int n, int bs) {
 void eval_tail(const pswe_plan& P, const pswe_params& prm, const double2* proj, const double2* state,
                double2* f_imp, double2* f_exp, int n_batch, cudaStream_t st) {
     if (n_batch <= 0) return;
-    eval_tail_kernel<<<grid_k(P.R, n_batch, 128), 128, 0, st>>>(P.R, P.d_eps, proj, state, f_imp, f_exp,
+    launch_pdl(eval_tail_kernel, grid_k(P.R, n_batch, 128), dim3(128), 0, st, P.R, P.d_eps, proj, state, f_imp, f_exp,
                                                                 1.0 / (prm.radius * prm.radius), prm.phi_bar,
                                                                 prm.nu);
     PSWE_LAUNCH_CHECK();

@@ -170,6 +170,13 @@ static void plan_free(pswe_plan* p) {
         if (q) cudaFree(q);
 }
 
+namespace pswe {
+bool pdl_enabled() {
+    static const bool on = [] { const char* e = std::getenv("PSWE_NO_PDL"); return !(e && std::atoi(e) != 0); }();
+    return on;
+}
+}  // namespace pswe
+
 template <class T>
 static T* upload(const std::vector<T>& v) {
     T* d = nullptr;

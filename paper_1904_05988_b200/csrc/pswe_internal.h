@@ -40,6 +40,32 @@ int guarded(F&& f) {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Programmatic dependent launch (PDL) of the eval chain prep -> inverse -> grid stage -> forward
+// -> tail: each kernel is launched with programmatic stream serialisation, runs its independent
+// prologue (mbarrier init, plan tables, twiddles), calls pdl_wait() before touching its
+// predecessor's output (every thread of every kernel waits, so completion stays transitive) and
+// pdl_trigger() early, so the next kernel's blocks become resident during this kernel's tail.
+// Without the launch attribute both instructions are no-ops. PSWE_NO_PDL=1 disables it.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
+#endif
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    PSWE_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // ------------------------------------------------------------------------------------------
 // spectral indexing (field.hpp:29-32) and the "extended" triangle s = m..R+1 used internally
 
