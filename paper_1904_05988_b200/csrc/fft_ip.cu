@@ -86,6 +86,17 @@ __host__ __device__ constexpr int ip_ntw(int N) { return ip_off(N, ip_npass(N));
 __device__ __forceinline__ int ipad(int i) { return i + (i >> 3); }
 __host__ __device__ constexpr int ipadded(int n) { return n + (n >> 3); }
 
+// w[k] = w1^k, k = 1..P-1, from the one root w1 = w_n^j read from the table: squares for even k,
+// one more factor w1 for odd k (product depth <= log2(k) + 1; a few ulp). Trades P-2 shared-memory
+// twiddle reads per butterfly (the FFT stage is shared-memory-bandwidth bound) for FP64 work.
+template <int P>
+__device__ __forceinline__ void pass_roots(double2 (&w)[P], double2 w1) {
+    w[0] = make_double2(1.0, 0.0);
+    if constexpr (P > 1) w[1] = w1;
+#pragma unroll
+    for (int k = 2; k < P; ++k) w[k] = (k & 1) ? cmul(w[k - 1], w1) : cmul(w[k >> 1], w[k >> 1]);
+}
+
 // DIF pass s on G rows of A: sub-blocks of length n, butterflies over t (stride M), then the
 // twiddle w_n^(j k) on output k; outputs back to the same slots.
 template <int N, int s, int G, bool INV>
@@ -98,17 +109,14 @@ __device__ __forceinline__ void dif_pass(double2* A, const double2* TW) {
         double2 v[P];
 #pragma unroll
         for (int t = 0; t < P; ++t) v[t] = A[ipad(base + t * M)];
-        double2 w[P > 1 ? P - 1 : 1];
-        if constexpr (M > 1) {
-#pragma unroll
-            for (int k = 1; k < P; ++k) w[k - 1] = TW[OFF + (k - 1) * M + j];
-        }
+        double2 w[P];
+        if constexpr (M > 1) pass_roots<P>(w, TW[OFF + j]);
         dft<P, INV>(v);
         A[ipad(base)] = v[0];
 #pragma unroll
         for (int k = 1; k < P; ++k) {
             double2 o = v[k];
-            if constexpr (M > 1) o = cmul(o, INV ? cconj(w[k - 1]) : w[k - 1]);
+            if constexpr (M > 1) o = cmul(o, INV ? cconj(w[k]) : w[k]);
             A[ipad(base + k * M)] = o;
         }
     }
@@ -126,11 +134,10 @@ __device__ __forceinline__ void dit_pass(double2* A, const double2* TW) {
 #pragma unroll
         for (int t = 0; t < P; ++t) v[t] = A[ipad(base + t * M)];
         if constexpr (M > 1) {
+            double2 w[P];
+            pass_roots<P>(w, TW[OFF + j]);
 #pragma unroll
-            for (int t = 1; t < P; ++t) {
-                const double2 w = TW[OFF + (t - 1) * M + j];
-                v[t] = cmul(v[t], INV ? cconj(w) : w);
-            }
+            for (int t = 1; t < P; ++t) v[t] = cmul(v[t], INV ? cconj(w[t]) : w[t]);
         }
         dft<P, INV>(v);
 #pragma unroll
@@ -193,14 +200,15 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
 
     // load + pre-pass: task (f, k), k = 0..N/2, owns Z_k and Z_{N-k}; all loads issued first
     constexpr int H = N / 2 + 1;
-    constexpr int U = (4 * H + kIpThreads - 1) / kIpThreads;
+    constexpr int HS = (H + 7) & ~7;  // task stride per field: 8-aligned k runs (no bank conflicts)
+    constexpr int U = (4 * HS + kIpThreads - 1) / kIpThreads;
     double2 xa[U], xb[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int it = threadIdx.x + u * kIpThreads;
         xa[u] = xb[u] = make_double2(0.0, 0.0);
-        if (it < 4 * H) {
-            const int f = it / H, k = it - f * H;
+        const int f = it / HS, k = it - f * HS;
+        if (f < 4 && k < H) {
             if (k <= R) xa[u] = in[f * rowsz + k];
             if (k > 0 && N - k <= R) xb[u] = in[f * rowsz + N - k];
         }
@@ -208,8 +216,8 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int it = threadIdx.x + u * kIpThreads;
-        if (it < 4 * H) {
-            const int f = it / H, k = it - f * H;
+        const int f = it / HS, k = it - f * HS;
+        if (f < 4 && k < H) {
             double2 a = xa[u];
             if (k == 0) a.y = 0.0;  // Im G_0 := 0
             A[ipad(f * N + k)] = c2r_z(a, xb[u], __ldg(post + k));
