@@ -407,8 +407,9 @@ __global__ void xtile_prep_kernel(int R, int NQ, int SX, int nq, int nct, const 
     extern __shared__ double tile[];  // [CH][SX]
     const int cg = blockIdx.x, z = blockIdx.y;
     const int tl = threadIdx.x & (CH - 1), bl = threadIdx.x / CH;
-    const int m = chunk_m[cg];
-    const int t = (cg - cbase[m]) * CH + tl;
+    const int2 mc = reinterpret_cast<const int2*>(chunk_m)[cg];  // (m, chunk within m): one load
+    const int m = mc.x;
+    const int t = mc.y * CH + tl;
     const int s = m + t;
     const int item = (z * NQ) / PER + bl;
     const long K = (long)(R + 1) * (R + 2) / 2;
@@ -690,11 +691,11 @@ void build_legendre_table2(pswe_plan& P) {
     const size_t n = (size_t)off[P.R + 1] * Jp * 16;
     PSWE_CUDA(cudaMalloc(&P.d_ptab2, n * sizeof(double)));
     P.n_chunks = off[P.R + 1];
-    std::vector<int> cm(P.n_chunks);
+    std::vector<int2> cm(P.n_chunks);
     for (int m = 0; m <= P.R; ++m)
-        for (int c = off[m]; c < off[m + 1]; ++c) cm[c] = m;
-    PSWE_CUDA(cudaMalloc(&P.d_chunk_m, cm.size() * sizeof(int)));
-    PSWE_CUDA(cudaMemcpy(P.d_chunk_m, cm.data(), cm.size() * sizeof(int), cudaMemcpyHostToDevice));
+        for (int c = off[m]; c < off[m + 1]; ++c) cm[c] = make_int2(m, c - off[m]);
+    PSWE_CUDA(cudaMalloc(&P.d_chunk_m, cm.size() * sizeof(int2)));
+    PSWE_CUDA(cudaMemcpy(P.d_chunk_m, cm.data(), cm.size() * sizeof(int2), cudaMemcpyHostToDevice));
     // forward tasks: all (m, chunk) in pair order m, R-m, m+1, R-m-1, ... (equal work per pair) cut
     // into contiguous runs of at most two orders that fit kFwdWarps warps x kFwdCpw chunk slots
     // (each order's run starts on a warp boundary), about kFwdPerSm runs per SM, so that one wave

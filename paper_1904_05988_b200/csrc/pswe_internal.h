@@ -118,7 +118,7 @@ struct pswe_plan {
     int* d_chk_off = nullptr;    // [R+2] chunk offsets per m into d_chk
     double* d_ptab2 = nullptr;   // STREAM mode: P tiles [m][chunk][Jp][16] swizzled (legendre_stream.cu)
     int n_chunks = 0;            // STREAM mode: 16-degree chunks over all m (= d_chk_off[R+1])
-    int* d_chunk_m = nullptr;    // STREAM mode: [n_chunks] order m of each chunk
+    int* d_chunk_m = nullptr;    // STREAM mode: [n_chunks] int2 (order m, chunk within m)
     mutable double* d_xtile = nullptr;  // STREAM mode: inverse X tiles (grow-only scratch)
     mutable size_t xtile_cap = 0;       // doubles
     int4* d_fwd_ta = nullptr;     // STREAM mode: forward tasks (m_a, first chunk, chunks of m_a, m_b)
