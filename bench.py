@@ -4,7 +4,9 @@
 Headline metric (BASELINE.json): SWE RHS evals/s (fp64 SH fwd+inv) at T255.
   step  = one explicit+implicit right-hand-side evaluation (eval_nonlinear + eval_linear,
           swe.cpp:9-69) of B = 5 T255 states (the 5 fine SDC nodes of config 3; refresh of all
-          nodes after prediction/restriction), on the reference's own T255 grid 384 x 768.
+          nodes after prediction/restriction) on BASELINE's T255 grid 256 x 512 (configs[1] and
+          the fine level of configs[2]); the reference's dealiased grid 384 x 768 is reported
+          beside it (dealiased_grid).
   value = evals/s over the whole job (all ranks; each rank evaluates its own states: weak).
   L2    = flushed (256 MiB write) between timed steps, outside the event-timed span.
 Side results on the same JSON line:
@@ -16,7 +18,7 @@ Side results on the same JSON line:
                  grid stage and the tail; every stage is listed under roofline.stages;
   cpu_baseline   the reference (oracle/_ref, compiled from /root/reference) timed on the host
                  cores, rank 0 at N=1 only;
-  pfasst         config-3-shape PFASST block (T255/T127, 5/3 nodes, dt 60 s, 8 steps, 4 its),
+  pfasst         config-3 PFASST block (T255 256x512 / T127 128x256, 5/3 nodes, dt 60 s, 8 steps, 4 its),
                  n_ts = N time ranks (NCCL) — wall s per simulated day;
   transform      config-2 micro-bench: 15-field round trip at T255 on 256 x 512.
 --impl reference times the reference's CPU path (oracle/_ref) on the same workload.
@@ -38,7 +40,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SWE RHS evals/s (fp64 SH fwd+inv) at T255"
-R_BENCH, NLAT, NLON, BATCH = 255, 384, 768, 5
+R_BENCH, NLAT, NLON, BATCH = 255, 256, 512, 5
+NLAT_DEALIASED, NLON_DEALIASED = 384, 768
 
 
 def parse():
@@ -72,7 +75,7 @@ def reference_eval_rate(seconds: float, threads: int | None = None):
     if threads:
         ref.lib().ref_set_threads(threads)
     cores = ref.lib().ref_max_threads()
-    plan = ref.RefPlan(R_BENCH)  # reference dealiased grid 384 x 768
+    plan = ref.RefPlan(R_BENCH, NLAT, NLON)
     st = bench_states(n=1)[0]
     p = ModelParams(phi_bar=9.80616 * 1e4)
     ref.lib()  # noqa
@@ -84,7 +87,7 @@ def reference_eval_rate(seconds: float, threads: int | None = None):
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    return n / el, cores, f"{n} sequential eval_nonlinear+eval_linear calls at T255 384x768 ({el:.1f} s)"
+    return n / el, cores, f"{n} sequential eval_nonlinear+eval_linear calls at T255 {NLAT}x{NLON} ({el:.1f} s)"
 
 
 def run_reference_arm(args):
@@ -96,7 +99,7 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpintswe_ref.so not built"}))
         return
     from oracle.pswe_oracle import ModelParams
-    plan = ref.RefPlan(R_BENCH)
+    plan = ref.RefPlan(R_BENCH, NLAT, NLON)
     states = bench_states()
     p = ModelParams(phi_bar=9.80616 * 1e4)
     cores = ref.lib().ref_max_threads()
@@ -248,6 +251,26 @@ def run_ours(args):
     sequential = {"value": BATCH * args.steps / (seq_ms * 1e-3), "unit": "evals/s",
                   "us_per_eval": 1e3 * seq_ms / (BATCH * args.steps),
                   "note": "one state per call, back to back (as inside an SDC sweep)"}
+
+    # the same batch on the reference's dealiased T255 grid 384 x 768 (side result)
+    dplan = P.TransformPlan(R_BENCH, NLAT_DEALIASED, NLON_DEALIASED, args.legendre)
+    dplan.reserve(BATCH)
+    for _ in range(3):
+        _lib.check(L.pswe_eval_imex(dplan.handle, ctypes.byref(cprm), states.data_ptr(), fi.data_ptr(),
+                                    fe.data_ptr(), BATCH, _stream()))
+    dms = 0.0
+    for k in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.check(L.pswe_eval_imex(dplan.handle, ctypes.byref(cprm), states.data_ptr(), fi.data_ptr(),
+                                    fe.data_ptr(), BATCH, _stream()))
+        b.record()
+        torch.cuda.synchronize()
+        dms += a.elapsed_time(b)
+    dealiased = {"grid": f"{NLAT_DEALIASED}x{NLON_DEALIASED}", "value": BATCH * args.steps / (dms * 1e-3),
+                 "unit": "evals/s", "ms_per_step": dms / args.steps}
+    del dplan
 
     # per-kernel durations (same workload, L2 flushed) for the roofline
     stage = np.zeros(4)
@@ -405,6 +428,7 @@ def run_ours(args):
                        "parallelism": f"{world} rank(s), independent states per rank"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": gpu_launches,
             "transform": transform, "pfasst": pf_res, "sequential_single_state": sequential,
+            "dealiased_grid": dealiased,
         }
         print(json.dumps(line))
     if world > 1:
@@ -413,7 +437,7 @@ def run_ours(args):
 
 
 def run_pfasst(P, prm, world, rank, dev, clocks_dev=0):
-    """Config-3 shape: T255 (384x768) / T127 (192x384), 5/3 nodes, dt 60 s, 8 steps, 4 its."""
+    """Config 3: T255 (256x512) / T127 (128x256), 5/3 nodes, dt 60 s, 8 steps, 4 iterations."""
     import torch
     import torch.distributed as dist
 
@@ -422,8 +446,8 @@ def run_pfasst(P, prm, world, rank, dev, clocks_dev=0):
     if steps % world:
         return {"skipped": f"8 steps not divisible by {world} ranks"}
     n_blocks = steps // world
-    pf_plan = P.TransformPlan(255)
-    pc_plan = P.TransformPlan(127)
+    pf_plan = P.TransformPlan(255, 256, 512)
+    pc_plan = P.TransformPlan(127, 128, 256)
     fine, coarse = P.Level(pf_plan, prm, 5), P.Level(pc_plan, prm, 3)
     pair = P.TransferPair(fine, coarse)
     cfg = P.BlockConfig(world, dt, n_iter)
@@ -449,7 +473,7 @@ def run_pfasst(P, prm, world, rank, dev, clocks_dev=0):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     wall = ms * 1e-3
-    return {"config": "config 3 shape: T255(384x768)/T127(192x384), 5/3 nodes, dt 60 s, 8 steps, 4 iterations",
+    return {"config": "config 3: T255(256x512)/T127(128x256), 5/3 nodes, dt 60 s, 8 steps, 4 iterations",
             "n_ts": world, "blocks": n_blocks, "wall_s": wall, "wall_s_per_sim_day": wall / (steps * dt) * 86400,
             "final_residuals": [float(r) for r in hist[-1][:, -1]]}
 

@@ -621,22 +621,16 @@ void fwd_launch(const pswe_plan& P, const double2* four, int nq, double2* out, b
 constexpr int kInvStages = PSWE_INV_STAGES;  // ring stages (one chunk each)
 constexpr int kInvSlices = PSWE_INV_SLICES;  // latitude slices per block (two warps each)
 
-// column tiles per group for nq complex columns. Measured (tools/stage_times.py): NT = 5 (one
-// group of 20 columns, 0.45 fragment loads per DMMA) wins for a 5-state batch once there are
-// >= 192 latitude pairs to fill the machine; otherwise the fewest padded n-tiles, then the fewest
-// groups (each group re-streams the P table).
+// column tiles per group for nq complex columns. Measured for the TMA kernel
+// (tools/stage_times.py, 5-state batch, 20 columns): NT = 2 at 128 latitude pairs (40.0 us vs 45-47
+// for NT = 1, 4, 5), NT = 3 at 192 (51.9 vs 54-59): small NT keeps registers low (more resident
+// warps) and gives more, better-balanced blocks; the extra P re-reads hit L2. One tile for <= 4
+// columns. PSWE_INV_NT overrides (tuning only).
 int inv_choose_nt(const pswe_plan& P, int nq) {
-    if (nq >= 20 && nq % 20 == 0 && P.J >= 192) return 5;
-    int best = 1, best_cost = 1 << 30;
-    for (int nt = 4; nt >= 1; --nt) {
-        const int groups = (nq + 4 * nt - 1) / (4 * nt);
-        const int cost = groups * nt * 8 + groups;
-        if (cost < best_cost) {
-            best_cost = cost;
-            best = nt;
-        }
-    }
-    return best;
+    static const int forced = [] { const char* e = getenv("PSWE_INV_NT"); return e ? atoi(e) : 0; }();
+    if (forced >= 1 && forced <= 5) return forced;
+    if (nq <= 4) return 1;
+    return P.J >= 192 ? 3 : 2;
 }
 
 template <int NT>
