@@ -393,25 +393,29 @@ void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out,
 // X tiles: per column group z (4 NT complex columns from q0 = 4 NT z), per chunk (cbase(m) + c):
 // [16 degrees tl][8 NT + 2] doubles, column 2 ql + {re, im}, two zero pad columns; degree
 // t = 16 c + tl of order m (extended t = 0..R+1-m; standard t = 0..R-m), zero beyond.
-// prep: block (chunk, z), thread (item bl, degree tl) with the degree fastest (coalesced reads
-// of the m-major coefficient rows) computes all PER columns of its item (transform.cpp:204-206
-// with the H-sums as P-sums): EVAL item = state, columns {Phi, zeta, U, V}; UV item = pair,
-// columns {U, V}; PLAIN item = field (standard layout, copied). The tile is assembled in shared
-// memory and stored as one contiguous block.
+// prep: block (chunk, item group), thread (item, degree tl) with the degree fastest (coalesced
+// reads of the m-major coefficient rows) computes all PER columns of its item (transform.cpp:
+// 204-206 with the H-sums as P-sums): EVAL item = state, columns {Phi, zeta, U, V}; UV item =
+// pair, columns {U, V}; PLAIN item = field (standard layout, copied), and stores them into the
+// tile of whichever column group they fall in. One block per chunk for every column tiling; the
+// threads of item slot g < groups also zero tile g's pad columns and the columns past nq.
+constexpr int kPrepItems = 32;  // items per block (blockIdx.y covers more)
 template <int KIND>
-__global__ void xtile_prep_kernel(int R, int NQ, int SX, int nq, int nct, const int* __restrict__ chunk_m,
-                                  const int* __restrict__ cbase, const double* __restrict__ eps,
-                                  const double* __restrict__ rtab, const double2* __restrict__ in,
-                                  const double2* __restrict__ in2, double radius, double* __restrict__ Xt) {
+__global__ void __launch_bounds__(CH * kPrepItems)
+    xtile_prep_kernel(int R, int NQ, int SX, int nq, int nct, const int* __restrict__ chunk_desc,
+                      const double* __restrict__ eps, const double* __restrict__ rtab,
+                      const double2* __restrict__ in, const double2* __restrict__ in2, double radius,
+                      double* __restrict__ Xt) {
     constexpr int PER = KIND == INV_EVAL ? 4 : (KIND == INV_UV ? 2 : 1);
-    extern __shared__ double tile[];  // [CH][SX]
-    const int cg = blockIdx.x, z = blockIdx.y;
-    const int tl = threadIdx.x & (CH - 1), bl = threadIdx.x / CH;
-    const int2 mc = reinterpret_cast<const int2*>(chunk_m)[cg];  // (m, chunk within m): one load
+    const int cg = blockIdx.x;
+    const int tl = threadIdx.x & (CH - 1), il = threadIdx.x / CH;
+    const int item = blockIdx.y * kPrepItems + il;
+    const int nitems = (nq + PER - 1) / PER;
+    const int groups = (nq + NQ - 1) / NQ;
+    const int2 mc = reinterpret_cast<const int2*>(chunk_desc)[cg];  // (m, chunk within m)
     const int m = mc.x;
     const int t = mc.y * CH + tl;
     const int s = m + t;
-    const int item = (z * NQ) / PER + bl;
     const long K = (long)(R + 1) * (R + 2) / 2;
     const long bs = off_std(R, m), bx = off_ext(R, m);
     double2 v[PER];
@@ -419,7 +423,7 @@ __global__ void xtile_prep_kernel(int R, int NQ, int SX, int nq, int nct, const 
     for (int f = 0; f < PER; ++f) v[f] = make_double2(0.0, 0.0);
     pdl_trigger();
     pdl_wait();  // the states come from the preceding kernel
-    if (bl * PER < NQ && item * PER < nq) {
+    if (item < nitems) {
         if (KIND == INV_PLAIN) {
             if (s <= R) v[0] = in[(long)item * K + bs + t];
         } else if (s <= R + 1) {
@@ -446,22 +450,21 @@ __global__ void xtile_prep_kernel(int R, int NQ, int SX, int nq, int nct, const 
             v[o] = make_double2(inv_a * (-m * chi.y - cpsi.x), inv_a * (m * chi.x - cpsi.y));
             v[o + 1] = make_double2(inv_a * (-m * psi.y + cchi.x), inv_a * (m * psi.x + cchi.y));
         }
-    }
-    if (bl * PER < NQ) {
 #pragma unroll
         for (int f = 0; f < PER; ++f) {
-            tile[tl * SX + 2 * (bl * PER + f)] = v[f].x;
-            tile[tl * SX + 2 * (bl * PER + f) + 1] = v[f].y;
+            const int q = item * PER + f;
+            if (q < nq) {
+                const int z = q / NQ, ql = q - z * NQ;
+                double* row = Xt + ((long)z * nct + cg) * CH * SX + (long)tl * SX;
+                *reinterpret_cast<double2*>(row + 2 * ql) = v[f];
+            }
         }
     }
-    if (threadIdx.x < CH) {
-        tile[threadIdx.x * SX + 2 * NQ] = 0.0;
-        tile[threadIdx.x * SX + 2 * NQ + 1] = 0.0;
+    for (int z = blockIdx.y * kPrepItems + il; z < groups; z += gridDim.y * kPrepItems) {
+        double* row = Xt + ((long)z * nct + cg) * CH * SX + (long)tl * SX;
+        for (int c = 2 * max(0, min(NQ, nq - z * NQ)); c < SX; c += 2)
+            *reinterpret_cast<double2*>(row + c) = make_double2(0.0, 0.0);
     }
-    __syncthreads();
-    double2* dst = reinterpret_cast<double2*>(Xt + ((long)z * nct + cg) * CH * SX);
-    const double2* src = reinterpret_cast<const double2*>(tile);
-    for (int i = threadIdx.x; i < CH * SX / 2; i += blockDim.x) dst[i] = src[i];
 }
 
 // grid (ceil(nslices / WS), R+1, column groups); 2 WS warps per block: warps 2w, 2w+1 share
@@ -774,22 +777,24 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
         PSWE_CUDA(cudaMalloc(&P.d_xtile, need * sizeof(double)));
         P.xtile_cap = need;
     }
-    dim3 g(P.n_chunks, groups);
     const int per = kind == INV_EVAL ? 4 : (kind == INV_UV ? 2 : 1);
-    const int nthr = CH * ((NQ + per - 1) / per);
-    const size_t tsm = (size_t)CH * SX * sizeof(double);
+    const int nitems = (nq + per - 1) / per;
+    const int span = std::max(nitems, groups);  // item slots also zero the groups' pad columns
+    const int iy = (span + kPrepItems - 1) / kPrepItems;
+    const int ipb = std::min(span, kPrepItems);
+    dim3 g(P.n_chunks, iy);
 #ifdef PSWE_DIAG_NOPREP
     if (false)
 #endif
     if (kind == INV_EVAL)
-        launch_pdl(xtile_prep_kernel<INV_EVAL>, g, dim3(nthr), tsm, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
-                                                          P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
+        launch_pdl(xtile_prep_kernel<INV_EVAL>, g, dim3(CH * ipb), 0, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m,
+                   P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     else if (kind == INV_UV)
-        launch_pdl(xtile_prep_kernel<INV_UV>, g, dim3(nthr), tsm, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
-                                                        P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
+        launch_pdl(xtile_prep_kernel<INV_UV>, g, dim3(CH * ipb), 0, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m,
+                   P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     else
-        launch_pdl(xtile_prep_kernel<INV_PLAIN>, g, dim3(nthr), tsm, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m, P.d_chk_off,
-                                                           P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
+        launch_pdl(xtile_prep_kernel<INV_PLAIN>, g, dim3(CH * ipb), 0, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m,
+                   P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     PSWE_LAUNCH_CHECK();
 #ifdef PSWE_DIAG_NOINV
     return;
