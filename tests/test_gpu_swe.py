@@ -71,6 +71,22 @@ def test_batched_equals_single(P):
         np.testing.assert_array_equal(batch[i], single)
 
 
+@pytest.mark.parametrize("n", [6, 7, 11])
+@pytest.mark.parametrize("R,grid", [(63, (96, 192)), (255, (256, 512))])
+def test_large_batches_equal_single(P, R, grid, n):
+    """Batches above 5 states split into several column groups (G tiles of <= 5 states, inverse
+    X tiles of 4 NT columns): every state must match its own single-state evaluation."""
+    from paper_1904_05988_b200.cases import balanced_random_state
+    plan = P.TransformPlan(R, grid[0], grid[1])
+    p = P.ModelParams(phi_bar=9.80616 * 1e4)
+    sts = np.stack([balanced_random_state(R, 40.0, 100 + s, phi_bar=p.phi_bar) for s in range(n)])
+    fi_b, fe_b = (host(t) for t in P.imex_split(cuda(sts), p, plan))
+    for i in range(n):
+        fi, fe = (host(t) for t in P.imex_split(cuda(sts[i:i + 1]), p, plan))
+        assert rel_diff_fields(fe_b[i], fe[0]) < 1e-13
+        assert rel_diff_fields(fi_b[i], fi[0]) < 1e-15
+
+
 def test_nonlinear_properties(P):
     """test_swe.cpp:75-129."""
     R = 15
