@@ -133,6 +133,10 @@ int pswe_interpolate_space(int rc, int rf, const double* x, double* y, int n_sta
 int pswe_restrict_states(pswe_pair* pair, void* stream);
 /* tau (device, coarse num_nodes states) := fas_correction(fine, coarse) (multilevel.cpp:109-137) */
 int pswe_fas_correction(pswe_pair* pair, double dt, double* tau, void* stream);
+/* multi-level FAS (Eq. 19): tau := fas_correction(fine, coarse) + R tau_fine,
+ * where tau_fine (device, fine num_nodes states, may be NULL) is the fine level's own FAS term
+ * (three-level chains; the reference itself is two-level, tau_fine = 0) */
+int pswe_fas_correction_ml(pswe_pair* pair, double dt, const double* tau_fine, double* tau, void* stream);
 /* save a copy of the coarse space-time state (pfasst.cpp:158) */
 int pswe_save_coarse(pswe_pair* pair, void* stream);
 /* fine.{state,f_imp,f_exp} += interpolate_increment(coarse - saved) (multilevel.cpp:139-150,
@@ -161,6 +165,15 @@ int pswe_pfasst_create_serial(pswe_pair* pair, const pswe_block_config* cfg, psw
 int pswe_pfasst_create_nccl(pswe_pair* pair, const pswe_block_config* cfg, int rank, int world,
                             const void* nccl_unique_id, pswe_pfasst** out);
 int pswe_nccl_unique_id(void* out128);
+/* Three-level PFASST (BASELINE config 4; the reference implements two levels only,
+ * multilevel.hpp:29-35): fine_mid = (fine, mid), mid_coarse = (mid, coarse) with
+ * mid_coarse->fine == fine_mid->coarse. Each iteration is a V-cycle fine -> mid -> coarse -> mid
+ * -> fine with the FAS of Eq. 19 on the mid and coarse levels; messages on three levels
+ * (0 fine, 1 mid, 2 coarse; step 'M' for the mid down-sweep). */
+int pswe_pfasst3_create_serial(pswe_pair* fine_mid, pswe_pair* mid_coarse, const pswe_block_config* cfg,
+                               pswe_pfasst** out);
+int pswe_pfasst3_create_nccl(pswe_pair* fine_mid, pswe_pair* mid_coarse, const pswe_block_config* cfg, int rank,
+                             int world, const void* nccl_unique_id, pswe_pfasst** out);
 int pswe_pfasst_destroy(pswe_pfasst* pf);
 /* Runs one block from theta0 (device, fine state). On return:
  *   final_state (device): fine last-node state of the LAST time step of the block (the
@@ -176,6 +189,8 @@ int pswe_pfasst_messages(const pswe_pfasst* pf, int* out, int max_records);
  * csrc/pfasst.cpp OpCode (worker_predict / worker_iterate, pfasst.cpp:78-176). Returns the op
  * count; writes at most max_ops ops. Host-only (no device work). */
 int pswe_pfasst_schedule(int w, int n_time_steps, int n_iter, int* out, int max_ops);
+/* the same for a chain of n_levels = 2 or 3 levels (returns -1 otherwise) */
+int pswe_pfasst_schedule_ml(int n_levels, int w, int n_time_steps, int n_iter, int* out, int max_ops);
 
 /* FP64 throughput microbenchmark on the current device (roofline denominator; MEASURED_PEAKS.json
  * has no FP64 figure): use_dmma = 0 -> DFMA, 1 -> DMMA m8n8k4. Returns TFLOP/s (< 0 on error). */

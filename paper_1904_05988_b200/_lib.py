@@ -68,16 +68,20 @@ SIGNATURES = {
     "pswe_interpolate_space": (_i, [_i, _i, _vp, _vp, _i, _vp]),
     "pswe_restrict_states": (_i, [_vp, _vp]),
     "pswe_fas_correction": (_i, [_vp, _d, _vp, _vp]),
+    "pswe_fas_correction_ml": (_i, [_vp, _d, _vp, _vp, _vp]),
     "pswe_save_coarse": (_i, [_vp, _vp]),
     "pswe_interpolate_increment_add": (_i, [_vp, _vp, _vp]),
     "pswe_interpolate_states": (_i, [_vp, _vp]),
     "pswe_pfasst_create_serial": (_i, [_vp, ctypes.POINTER(BlockConfig), ctypes.POINTER(_vp)]),
     "pswe_pfasst_create_nccl": (_i, [_vp, ctypes.POINTER(BlockConfig), _i, _i, _vp, ctypes.POINTER(_vp)]),
+    "pswe_pfasst3_create_serial": (_i, [_vp, _vp, ctypes.POINTER(BlockConfig), ctypes.POINTER(_vp)]),
+    "pswe_pfasst3_create_nccl": (_i, [_vp, _vp, ctypes.POINTER(BlockConfig), _i, _i, _vp, ctypes.POINTER(_vp)]),
     "pswe_nccl_unique_id": (_i, [_vp]),
     "pswe_pfasst_destroy": (_i, [_vp]),
     "pswe_pfasst_run_block": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "pswe_pfasst_messages": (_i, [_vp, _pi, _i]),
     "pswe_pfasst_schedule": (_i, [_i, _i, _i, _pi, _i]),
+    "pswe_pfasst_schedule_ml": (_i, [_i, _i, _i, _i, _pi, _i]),
     "pswe_fp64_peak": (_d, [_i, _i]),
     "pswe_eval_imex_timed": (_i, [_vp, ctypes.POINTER(Params), _vp, _vp, _vp, _i, _vp,
                                   ctypes.POINTER(ctypes.c_float)]),

@@ -32,7 +32,7 @@ void level_refresh(pswe_level* L, int first, int count, cudaStream_t st);
 void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st);
 void level_residual(pswe_level* L, double dt, double* out, cudaStream_t st);
 void pair_restrict_states(pswe_pair* P, cudaStream_t st);
-void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st);
+void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st, const double2* tau_f = nullptr);
 void pair_save(pswe_pair* P, cudaStream_t st);
 void pair_interp_increment_add(pswe_pair* P, double2* dstate0, cudaStream_t st);
 void pair_interp_states(pswe_pair* P, cudaStream_t st);
@@ -66,13 +66,32 @@ enum OpCode : int {
     OP_INTERP_INC = 15,        // fine.{state,F} += interpolate_increment(...)      :162-170
     OP_RECV_FINE_IC = 16,      // fine.state[0] = recv(fine_ch) + dstate[0]         :171-174
     OP_REFRESH_FINE0 = 17,     // refresh_node(fine, 0)                             :175
+    // three-level chain (config 4; the reference is two-level only, multilevel.hpp:29-35): a
+    // V-cycle per iteration, fine -> mid -> coarse -> mid -> fine, with the FAS of Eq. 19
+    // (tau_f != 0 on the mid level). Ops on the (fine, mid) pair reuse the
+    // two-level codes (RESTRICT, SAVE, INTERP_INC, INTERP_STATES); the coarse ops act on the
+    // coarsest level.
+    OP_INTERP_STATES_MC = 18,  // mid.state = interpolate_states(coarse.state)
+    OP_REFRESH_MID_ALL = 19,   // refresh all mid nodes
+    OP_RESTRICT_MC = 20,       // coarse.state = restrict_states(mid.state)
+    OP_SAVE_MC = 21,           // saved_mc = coarse
+    OP_FAS_MC = 22,            // tau_c = fas_correction(mid, coarse) + R tau_mid
+    OP_SWEEP_MID = 23,         // sweep(mid, tau_mid)
+    OP_SEND_MID = 24,          // send(mid.state[mm-1]) -> w+1
+    OP_INTERP_INC_MC = 25,     // mid.{state,F} += interpolate_increment(coarse - saved_mc)
+    OP_RECV_MID_IC = 26,       // mid.state[0] = recv(mid_ch), modes <= R_c from coarse.state[0]
+    OP_REFRESH_MID0 = 27,      // refresh_node(mid, 0)
+    OP_FAS_FM = 28,            // tau_mid = fas_correction(fine, mid)
 };
 
 struct Op {
     int code, phase, iter, arg;  // arg: use_tau for sweeps, residual index, message step char
 };
 
-std::vector<Op> build_schedule(int w, int n, int n_iter) {
+std::vector<Op> build_schedule3(int w, int n, int n_iter);
+
+std::vector<Op> build_schedule(int w, int n, int n_iter, int nlev = 2) {
+    if (nlev == 3) return build_schedule3(w, n, n_iter);
     std::vector<Op> ops;
     ops.push_back({OP_PREDICT_INIT, 0, 0, 0});
     for (int q = 0; q <= w; ++q) {
@@ -106,20 +125,74 @@ std::vector<Op> build_schedule(int w, int n, int n_iter) {
     return ops;
 }
 
+// Three levels: predictor on the coarsest level (pipelined as in the two-level case), states
+// interpolated up level by level; each iteration sweeps the fine level, restricts to the mid
+// level (FAS), sweeps it (down) and sends its end state, restricts to the coarse level (FAS with
+// R tau_mid), runs the pipelined coarse sweep, then goes back up: coarse increment -> mid, mid IC
+// from w-1 (low modes from the coarse node 0), mid sweep (up), mid increment -> fine, fine IC from
+// w-1 (low modes from the mid node 0).
+std::vector<Op> build_schedule3(int w, int n, int n_iter) {
+    std::vector<Op> ops;
+    ops.push_back({OP_PREDICT_INIT, 0, 0, 0});
+    for (int q = 0; q <= w; ++q) {
+        if (q >= 1) {
+            ops.push_back({OP_RECV_COARSE_IC, 0, q - 1, 0});
+            ops.push_back({OP_REFRESH_COARSE0, 0, q, 0});
+        }
+        ops.push_back({OP_SWEEP_COARSE, 0, q, 0});
+        if (w < n - 1) ops.push_back({OP_SEND_COARSE, 0, q, 'P'});
+    }
+    ops.push_back({OP_INTERP_STATES_MC, 0, 0, 0});
+    ops.push_back({OP_REFRESH_MID_ALL, 0, 0, 0});
+    ops.push_back({OP_INTERP_STATES, 0, 0, 0});
+    ops.push_back({OP_REFRESH_FINE_ALL, 0, 0, 0});
+    ops.push_back({OP_RESIDUAL, 0, 0, 0});
+    for (int k = 1; k <= n_iter; ++k) {
+        ops.push_back({OP_SWEEP_FINE, 1, k, 0});
+        ops.push_back({OP_RESIDUAL, 1, k, k});
+        if (k == n_iter) break;
+        if (w < n - 1) ops.push_back({OP_SEND_FINE, 1, k, 'A'});
+        ops.push_back({OP_RESTRICT, 1, k, 0});
+        ops.push_back({OP_REFRESH_MID_ALL, 1, k, 0});
+        ops.push_back({OP_SAVE, 1, k, 0});
+        ops.push_back({OP_FAS_FM, 1, k, 0});
+        ops.push_back({OP_SWEEP_MID, 1, k, 0});
+        if (w < n - 1) ops.push_back({OP_SEND_MID, 1, k, 'M'});
+        ops.push_back({OP_RESTRICT_MC, 1, k, 0});
+        ops.push_back({OP_REFRESH_COARSE_ALL, 1, k, 0});
+        ops.push_back({OP_SAVE_MC, 1, k, 0});
+        ops.push_back({OP_FAS_MC, 1, k, 0});
+        if (w > 0) ops.push_back({OP_RECV_COARSE_IC, 1, k, 0});
+        ops.push_back({OP_REFRESH_COARSE0, 1, k, 0});
+        ops.push_back({OP_SWEEP_COARSE, 1, k, 1});
+        if (w < n - 1) ops.push_back({OP_SEND_COARSE, 1, k, 'C'});
+        ops.push_back({OP_INTERP_INC_MC, 1, k, 0});
+        if (w > 0) ops.push_back({OP_RECV_MID_IC, 1, k, 0});
+        ops.push_back({OP_REFRESH_MID0, 1, k, 0});
+        ops.push_back({OP_SWEEP_MID, 1, k, 0});
+        ops.push_back({OP_INTERP_INC, 1, k, 0});
+        if (w > 0) ops.push_back({OP_RECV_FINE_IC, 1, k, 0});
+        ops.push_back({OP_REFRESH_FINE0, 1, k, 0});
+    }
+    return ops;
+}
+
 struct MsgRec {
     int phase, iteration, step, sender, receiver, level, node;
 };
 
 // Message log of a block (MessageRecord, pfasst.hpp:22-31), merged in the reference's order.
-std::vector<MsgRec> message_log(int n, int n_iter, int mf, int mc) {
+// Three levels: level 0 fine, 1 mid, 2 coarse; step 'M' for the mid down-sweep message.
+std::vector<MsgRec> message_log(int n, int n_iter, int mf, int mc, int nlev = 2, int mm = 0) {
     std::vector<MsgRec> log;
     for (int r = 1; r < n; ++r) log.push_back({0, 0, 'B', 0, r, 0, 0});
     for (int w = 0; w < n; ++w)
-        for (const Op& o : build_schedule(w, n, n_iter)) {
-            if (o.code == OP_SEND_COARSE) log.push_back({o.phase, o.iter, o.arg, w, w + 1, 1, mc - 1});
+        for (const Op& o : build_schedule(w, n, n_iter, nlev)) {
+            if (o.code == OP_SEND_COARSE) log.push_back({o.phase, o.iter, o.arg, w, w + 1, nlev - 1, mc - 1});
             if (o.code == OP_SEND_FINE) log.push_back({o.phase, o.iter, o.arg, w, w + 1, 0, mf - 1});
+            if (o.code == OP_SEND_MID) log.push_back({o.phase, o.iter, o.arg, w, w + 1, 1, mm - 1});
         }
-    auto rank = [](int s) { return s == 'B' ? 0 : s == 'P' ? 1 : s == 'A' ? 2 : 3; };
+    auto rank = [](int s) { return s == 'B' ? 0 : s == 'P' ? 1 : s == 'A' ? 2 : s == 'M' ? 3 : 4; };
     std::stable_sort(log.begin(), log.end(), [&](const MsgRec& a, const MsgRec& b) {
         return std::make_tuple(a.phase, a.iteration, a.sender, rank(a.step)) <
                std::make_tuple(b.phase, b.iteration, b.sender, rank(b.step));
@@ -184,10 +257,14 @@ using namespace pswe;
 // One block controller. Owns the comm objects and per-block device buffers; the levels and the
 // pair belong to the caller.
 struct pswe_pfasst {
-    pswe_pair* pair = nullptr;
-    pswe_level *fine = nullptr, *coarse = nullptr;
-    int Rf = 0, Rc = 0, mf = 0, mc = 0;
-    long Kf = 0, Kc = 0;
+    pswe_pair* pair = nullptr;   // (fine, next level)
+    pswe_pair* pair2 = nullptr;  // three levels: (mid, coarse)
+    int nlev = 2;
+    pswe_level *fine = nullptr, *coarse = nullptr, *mid = nullptr;
+    int Rf = 0, Rc = 0, mf = 0, mc = 0, Rm = 0, mm = 0;
+    long Kf = 0, Kc = 0, Km = 0;
+    double2* d_tau_mid = nullptr;      // [mm][3Km]
+    double2* d_dstate0_mid = nullptr;  // [3Km]
     pswe_block_config cfg{};
     bool distributed = false;
     int rank = 0, world = 1;
@@ -200,14 +277,15 @@ struct pswe_pfasst {
         int phase, iter, level;
     };
     std::map<std::pair<int, int>, std::deque<Msg>> queues;
-    std::vector<double2*> pool[2];  // free message buffers per level
+    std::vector<double2*> pool[3];  // free message buffers per level
     // NCCL
-    ncclComm_t comm[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [level][parity]
+    ncclComm_t comm[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};  // [level][parity]
     ncclComm_t world_comm = nullptr;
-    cudaStream_t send_stream[2] = {nullptr, nullptr};
-    std::vector<double2*> send_bufs[2];
-    std::vector<cudaEvent_t> send_done[2];
-    size_t send_next[2] = {0, 0};
+    cudaStream_t send_stream[3] = {nullptr, nullptr, nullptr};
+    std::vector<double2*> send_bufs[3];
+    std::vector<cudaEvent_t> send_done[3];
+    size_t send_next[3] = {0, 0, 0};
+    long K_of(int level) const { return level == 0 ? Kf : (level == nlev - 1 ? Kc : Km); }
     double* d_res_all = nullptr;
     // serial emulation replays the whole block as one CUDA graph (captured on the 2nd call,
     // after an eager call has sized every pool); theta0 is copied into d_theta first
@@ -223,14 +301,26 @@ namespace {
 
 size_t state_bytes(long K) { return (size_t)3 * K * sizeof(double2); }
 
-void init_common(pswe_pfasst* pf, pswe_pair* pair, const pswe_block_config* cfg) {
+void init_common(pswe_pfasst* pf, pswe_pair* pair, const pswe_block_config* cfg, pswe_pair* pair2 = nullptr) {
     if (!pair || !cfg) throw std::invalid_argument("pswe_pfasst: NULL argument");
     if (cfg->n_time_steps < 1) throw std::invalid_argument("run_block: need n_time_steps >= 1");
     if (cfg->n_iter < 1) throw std::invalid_argument("run_block: need n_iter >= 1");
+    if (pair2 && pair2->fine != pair->coarse)
+        throw std::invalid_argument("pswe_pfasst3: the second pair must start at the first pair's coarse level");
     pf->pair = pair;
+    pf->pair2 = pair2;
+    pf->nlev = pair2 ? 3 : 2;
     pf->cfg = *cfg;
     pf->fine = pair->fine;
-    pf->coarse = pair->coarse;
+    pf->coarse = pair2 ? pair2->coarse : pair->coarse;
+    if (pair2) {
+        pf->mid = pair->coarse;
+        pf->Rm = pf->mid->R;
+        pf->mm = pf->mid->nn;
+        pf->Km = num_coeffs(pf->Rm);
+        PSWE_CUDA(cudaMalloc(&pf->d_tau_mid, pf->mm * state_bytes(pf->Km)));
+        PSWE_CUDA(cudaMalloc(&pf->d_dstate0_mid, state_bytes(pf->Km)));
+    }
     pf->Rf = pf->fine->R;
     pf->mf = pf->fine->nn;
     pf->Rc = pf->coarse->R;
@@ -249,18 +339,19 @@ template <class SendF, class RecvF>
 void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, SendF&& send, RecvF&& recv) {
     const int n = pf->cfg.n_time_steps, N = pf->cfg.n_iter;
     const double dt = pf->cfg.dt;
-    pswe_level *F = pf->fine, *C = pf->coarse;
-    for (const Op& o : build_schedule(w, n, N)) {
+    pswe_level *F = pf->fine, *C = pf->coarse, *M = pf->mid;
+    const int lc = pf->nlev - 1;  // message level of the coarsest level
+    for (const Op& o : build_schedule(w, n, N, pf->nlev)) {
         switch (o.code) {
             case OP_PREDICT_INIT:
                 pswe_restrict_space(pf->Rf, pf->Rc, reinterpret_cast<const double*>(theta0),
                                     reinterpret_cast<double*>(st_ptr(C, 0)), 1, st);
                 level_spread(C, st_ptr(C, 0), st);
                 break;
-            case OP_RECV_COARSE_IC: recv(w, 1, o.phase, o.iter, st_ptr(C, 0), pf->Kc); break;
+            case OP_RECV_COARSE_IC: recv(w, lc, o.phase, o.iter, st_ptr(C, 0), pf->Kc); break;
             case OP_REFRESH_COARSE0: level_refresh(C, 0, 1, st); break;
             case OP_SWEEP_COARSE: level_sweep(C, dt, o.arg ? pf->d_tau : nullptr, st); break;
-            case OP_SEND_COARSE: send(w, 1, o.phase, o.iter, st_ptr(C, pf->mc - 1), pf->Kc); break;
+            case OP_SEND_COARSE: send(w, lc, o.phase, o.iter, st_ptr(C, pf->mc - 1), pf->Kc); break;
             case OP_INTERP_STATES: pair_interp_states(pf->pair, st); break;
             case OP_REFRESH_FINE_ALL: level_refresh(F, 0, pf->mf, st); break;
             case OP_RESIDUAL: level_residual(F, dt, pf->d_res + (size_t)w * (N + 1) + o.arg, st); break;
@@ -273,6 +364,17 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
             case OP_INTERP_INC: pair_interp_increment_add(pf->pair, pf->d_dstate0, st); break;
             case OP_RECV_FINE_IC: recv(w, 0, o.phase, o.iter, st_ptr(F, 0), pf->Kf); break;
             case OP_REFRESH_FINE0: level_refresh(F, 0, 1, st); break;
+            case OP_INTERP_STATES_MC: pair_interp_states(pf->pair2, st); break;
+            case OP_REFRESH_MID_ALL: level_refresh(M, 0, pf->mm, st); break;
+            case OP_RESTRICT_MC: pair_restrict_states(pf->pair2, st); break;
+            case OP_SAVE_MC: pair_save(pf->pair2, st); break;
+            case OP_FAS_MC: pair_fas(pf->pair2, dt, pf->d_tau, st, pf->d_tau_mid); break;
+            case OP_SWEEP_MID: level_sweep(M, dt, pf->d_tau_mid, st); break;
+            case OP_SEND_MID: send(w, 1, o.phase, o.iter, st_ptr(M, pf->mm - 1), pf->Km); break;
+            case OP_INTERP_INC_MC: pair_interp_increment_add(pf->pair2, pf->d_dstate0_mid, st); break;
+            case OP_RECV_MID_IC: recv(w, 1, o.phase, o.iter, st_ptr(M, 0), pf->Km); break;
+            case OP_REFRESH_MID0: level_refresh(M, 0, 1, st); break;
+            case OP_FAS_FM: pair_fas(pf->pair, dt, pf->d_tau_mid, st); break;
             default: throw std::logic_error("pfasst: unknown op");
         }
     }
@@ -283,9 +385,36 @@ __global__ void add_state_kernel(double2* dst, const double2* a, const double2* 
     if (i < n) dst[i] = make_double2(a[i].x + b[i].x, a[i].y + b[i].y);
 }
 
-void add_dstate0(pswe_pfasst* pf, double2* dst, const double2* msg, cudaStream_t st) {
-    const long n = 3 * pf->Kf;
-    add_state_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dst, msg, pf->d_dstate0, n);
+// received IC + the receiver's own interpolated node-0 increment (pfasst.cpp:171-174): the
+// reference's two-level form (fine level only). Three-level chains use low-mode replacement
+// instead (replace_low_modes below).
+bool has_dstate(const pswe_pfasst* pf, int level) { return level == 0 && pf->nlev == 2; }
+
+// Three-level IC update: node 0 of level l := received state with its coefficients (m, s) <= R_{l+1}
+// replaced by node 0 of level l+1, i.e. recv + pad(c0 - trunc(recv)). The two-level form above
+// measures the coarse increment against the OLD restricted node 0 while the received state is
+// already new, so the low-mode part of the IC change is counted twice; nested over two levels that
+// diverged (tests/test_gpu_pfasst3.py), while this form has the same fixed point without it.
+__global__ void replace_low_kernel(int Rf, int Rc, double2* __restrict__ dst, const double2* __restrict__ src) {
+    const int m = blockIdx.y, f = blockIdx.z;
+    const int s = m + blockIdx.x * blockDim.x + threadIdx.x;
+    if (s > Rc) return;
+    const long Kf = (long)(Rf + 1) * (Rf + 2) / 2, Kc = (long)(Rc + 1) * (Rc + 2) / 2;
+    dst[f * Kf + off_std(Rf, m) + (s - m)] = src[f * Kc + off_std(Rc, m) + (s - m)];
+}
+void replace_low_modes(pswe_pfasst* pf, int level, double2* dst, cudaStream_t st) {
+    pswe_level* lower = level == 0 ? pf->mid : pf->coarse;
+    const int Rf = level == 0 ? pf->Rf : pf->Rm;
+    const int Rc = lower->R;
+    dim3 grid((Rc + 1 + 127) / 128, Rc + 1, 3);
+    replace_low_kernel<<<grid, 128, 0, st>>>(Rf, Rc, dst, st_ptr(lower, 0));
+    PSWE_LAUNCH_CHECK();
+}
+bool has_low_replace(const pswe_pfasst* pf, int level) { return pf->nlev == 3 && level <= 1; }
+void add_dstate0(pswe_pfasst* pf, double2* dst, const double2* msg, cudaStream_t st, int level = 0) {
+    const long n = 3 * pf->K_of(level);
+    add_state_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dst, msg, level ? pf->d_dstate0_mid : pf->d_dstate0,
+                                                                  n);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -299,7 +428,7 @@ void run_serial(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
             b = pool.back();
             pool.pop_back();
         } else {
-            PSWE_CUDA(cudaMalloc(&b, state_bytes(level ? pf->Kc : pf->Kf)));
+            PSWE_CUDA(cudaMalloc(&b, state_bytes(pf->K_of(level))));
         }
         return b;
     };
@@ -315,8 +444,9 @@ void run_serial(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
         q.pop_front();
         if (m.phase != phase || m.iter != iter || m.level != level)
             throw std::logic_error("pfasst: message tag mismatch");
-        if (level == 0) add_dstate0(pf, dst, m.buf, st);
+        if (has_dstate(pf, level)) add_dstate0(pf, dst, m.buf, st, level);
         else PSWE_CUDA(cudaMemcpyAsync(dst, m.buf, state_bytes(K), cudaMemcpyDeviceToDevice, st));
+        if (has_low_replace(pf, level)) replace_low_modes(pf, level, dst, st);
         pf->pool[level].push_back(m.buf);  // stream-ordered reuse
     };
     for (int w = 0; w < pf->cfg.n_time_steps; ++w) run_worker(pf, w, theta0, st, send, recv);
@@ -347,11 +477,12 @@ void run_nccl(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
         // fine IC: receive into dst, then add the node-0 increment in place (pfasst.cpp:171-174)
         api.check(api.Recv(dst, state_bytes(K) / sizeof(double), ncclFloat64, w - 1, pf->comm[level][(w + 1) % 2], st),
                   "ncclRecv");
-        if (level == 0) add_dstate0(pf, dst, dst, st);
+        if (has_dstate(pf, level)) add_dstate0(pf, dst, dst, st, level);
+        if (has_low_replace(pf, level)) replace_low_modes(pf, level, dst, st);
     };
     run_worker(pf, w, theta0, st, send, recv);
     // make sure all sends are posted before the block ends
-    for (int l = 0; l < 2; ++l) {
+    for (int l = 0; l < pf->nlev; ++l) {
         cudaEvent_t e;
         PSWE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         PSWE_CUDA(cudaEventRecord(e, pf->send_stream[l]));
@@ -364,18 +495,28 @@ void run_nccl(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
 
 extern "C" {
 
+static void create_serial(pswe_pair* pair, pswe_pair* pair2, const pswe_block_config* cfg, pswe_pfasst** out) {
+    if (!out) throw std::invalid_argument("out is NULL");
+    auto* pf = new pswe_pfasst;
+    if (const char* e = std::getenv("PSWE_NO_GRAPH")) pf->use_graph = std::atoi(e) == 0;
+    try {
+        init_common(pf, pair, cfg, pair2);
+    } catch (...) {
+        delete pf;
+        throw;
+    }
+    *out = pf;
+}
+
 int pswe_pfasst_create_serial(pswe_pair* pair, const pswe_block_config* cfg, pswe_pfasst** out) {
+    return guarded([&] { create_serial(pair, nullptr, cfg, out); });
+}
+
+int pswe_pfasst3_create_serial(pswe_pair* fine_mid, pswe_pair* mid_coarse, const pswe_block_config* cfg,
+                               pswe_pfasst** out) {
     return guarded([&] {
-        if (!out) throw std::invalid_argument("out is NULL");
-        auto* pf = new pswe_pfasst;
-        if (const char* e = std::getenv("PSWE_NO_GRAPH")) pf->use_graph = std::atoi(e) == 0;
-        try {
-            init_common(pf, pair, cfg);
-        } catch (...) {
-            delete pf;
-            throw;
-        }
-        *out = pf;
+        if (!mid_coarse) throw std::invalid_argument("pswe_pfasst3: NULL mid-coarse pair");
+        create_serial(fine_mid, mid_coarse, cfg, out);
     });
 }
 
@@ -387,15 +528,15 @@ int pswe_nccl_unique_id(void* out128) {
     });
 }
 
-int pswe_pfasst_create_nccl(pswe_pair* pair, const pswe_block_config* cfg, int rank, int world,
-                            const void* uid, pswe_pfasst** out) {
-    return guarded([&] {
+static void create_nccl(pswe_pair* pair, pswe_pair* pair2, const pswe_block_config* cfg, int rank, int world,
+                        const void* uid, pswe_pfasst** out) {
+    {
         if (!out || !uid) throw std::invalid_argument("NULL argument");
         if (cfg && cfg->n_time_steps != world)
             throw std::invalid_argument("pswe_pfasst_create_nccl: n_time_steps must equal world size");
         auto& api = nccl();
         auto* pf = new pswe_pfasst;
-        init_common(pf, pair, cfg);
+        init_common(pf, pair, cfg, pair2);
         pf->distributed = true;
         pf->rank = rank;
         pf->world = world;
@@ -405,7 +546,7 @@ int pswe_pfasst_create_nccl(pswe_pair* pair, const pswe_block_config* cfg, int r
         ncclUniqueId base;
         std::memcpy(&base, uid, sizeof(base));
         api.check(api.CommInitRank(&pf->world_comm, world, base, rank), "ncclCommInitRank(world)");
-        for (int l = 0; l < 2; ++l)
+        for (int l = 0; l < pf->nlev; ++l)
             for (int p = 0; p < 2; ++p) {
                 // per-comm ids are broadcast through the world communicator
                 ncclUniqueId id;
@@ -418,10 +559,10 @@ int pswe_pfasst_create_nccl(pswe_pair* pair, const pswe_block_config* cfg, int r
                 cudaFree(d_id);
                 api.check(api.CommInitRank(&pf->comm[l][p], world, id, rank), "ncclCommInitRank(p2p)");
             }
-        for (int l = 0; l < 2; ++l) {
+        for (int l = 0; l < pf->nlev; ++l) {
             PSWE_CUDA(cudaStreamCreateWithFlags(&pf->send_stream[l], cudaStreamNonBlocking));
-            const long K = l ? pf->Kc : pf->Kf;
-            const int nslots = l ? world + cfg->n_iter + 2 : cfg->n_iter + 2;
+            const long K = pf->K_of(l);
+            const int nslots = l == pf->nlev - 1 ? world + cfg->n_iter + 2 : cfg->n_iter + 2;
             for (int s = 0; s < nslots; ++s) {
                 double2* b;
                 PSWE_CUDA(cudaMalloc(&b, state_bytes(K)));
@@ -434,6 +575,19 @@ int pswe_pfasst_create_nccl(pswe_pair* pair, const pswe_block_config* cfg, int r
         }
         PSWE_CUDA(cudaMalloc(&pf->d_res_all, sizeof(double) * world * (cfg->n_iter + 1)));
         *out = pf;
+    }
+}
+
+int pswe_pfasst_create_nccl(pswe_pair* pair, const pswe_block_config* cfg, int rank, int world,
+                            const void* uid, pswe_pfasst** out) {
+    return guarded([&] { create_nccl(pair, nullptr, cfg, rank, world, uid, out); });
+}
+
+int pswe_pfasst3_create_nccl(pswe_pair* fine_mid, pswe_pair* mid_coarse, const pswe_block_config* cfg, int rank,
+                             int world, const void* uid, pswe_pfasst** out) {
+    return guarded([&] {
+        if (!mid_coarse) throw std::invalid_argument("pswe_pfasst3: NULL mid-coarse pair");
+        create_nccl(fine_mid, mid_coarse, cfg, rank, world, uid, out);
     });
 }
 
@@ -448,9 +602,11 @@ int pswe_pfasst_destroy(pswe_pfasst* pf) {
         if (pf->ev_out) cudaEventDestroy(pf->ev_out);
         cudaFree(pf->d_tau);
         cudaFree(pf->d_dstate0);
+        if (pf->d_tau_mid) cudaFree(pf->d_tau_mid);
+        if (pf->d_dstate0_mid) cudaFree(pf->d_dstate0_mid);
         cudaFree(pf->d_res);
         if (pf->d_res_all) cudaFree(pf->d_res_all);
-        for (int l = 0; l < 2; ++l) {
+        for (int l = 0; l < 3; ++l) {
             for (auto* b : pf->pool[l]) cudaFree(b);
             for (auto* b : pf->send_bufs[l]) cudaFree(b);
             for (auto e : pf->send_done[l]) cudaEventDestroy(e);
@@ -551,7 +707,7 @@ int pswe_pfasst_run_block(pswe_pfasst* pf, const double* theta0, double* final_s
 
 int pswe_pfasst_messages(const pswe_pfasst* pf, int* out, int max_records) {
     if (!pf) return 0;
-    const auto log = message_log(pf->cfg.n_time_steps, pf->cfg.n_iter, pf->mf, pf->mc);
+    const auto log = message_log(pf->cfg.n_time_steps, pf->cfg.n_iter, pf->mf, pf->mc, pf->nlev, pf->mm);
     const int n = (int)log.size();
     if (out)
         for (int i = 0; i < n && i < max_records; ++i) {
@@ -565,7 +721,12 @@ int pswe_pfasst_messages(const pswe_pfasst* pf, int* out, int max_records) {
 
 // Schedule of worker w as 4 ints per op (code, phase, iter, arg); returns the op count.
 int pswe_pfasst_schedule(int w, int n_time_steps, int n_iter, int* out, int max_ops) {
-    const auto ops = build_schedule(w, n_time_steps, n_iter);
+    return pswe_pfasst_schedule_ml(2, w, n_time_steps, n_iter, out, max_ops);
+}
+
+int pswe_pfasst_schedule_ml(int n_levels, int w, int n_time_steps, int n_iter, int* out, int max_ops) {
+    if (n_levels != 2 && n_levels != 3) return -1;
+    const auto ops = build_schedule(w, n_time_steps, n_iter, n_levels);
     if (out)
         for (int i = 0; i < (int)ops.size() && i < max_ops; ++i) {
             out[4 * i] = ops[i].code;

@@ -255,6 +255,9 @@ __global__ void restrict_states_kernel(TimeMatArgs A, double2* const* __restrict
 
 // tau_i = dt * [ restrict(sum_j qfr(i,j)(FI_f[j] + FE_f[j])) - sum_j qc(i,j)(FI_c[j] + FE_c[j]) ]
 // (multilevel.cpp:109-137, same operation order)
+// Multi-level (Eq. 19): tau_c += R tau_f for a fine level that itself carries a
+// FAS term (three-level PFASST): the cumulative-form tau_f is restricted like a state (time matrix
+// tr at the coarse nodes, then spectral truncation).
 struct FasArgs {
     const double2* fi_f[kMaxNodes];
     const double2* fe_f[kMaxNodes];
@@ -262,6 +265,8 @@ struct FasArgs {
     const double2* fe_c[kMaxNodes];
     double qfr[kMaxNodes][kMaxNodes];
     double qc[kMaxNodes][kMaxNodes];
+    const double2* tau_f;  // nullable: [mf][3 Kf]
+    double tr[kMaxNodes][kMaxNodes];
     int mc, mf, Rf, Rc;
     double dt;
 };
@@ -284,7 +289,14 @@ __global__ void fas_kernel(FasArgs A, double2* tau) {
             axpy(acc, -w, A.fi_c[j][kc3]);
             axpy(acc, -w, A.fe_c[j][kc3]);
         }
-        tau[i * 3 * Kc + kc3] = make_double2(acc.x * A.dt, acc.y * A.dt);
+        double2 t = make_double2(acc.x * A.dt, acc.y * A.dt);
+        if (A.tau_f) {
+            for (int j = 0; j < A.mf; ++j) {
+                const double w = A.tr[i][j];
+                if (w != 0.0) axpy(t, w, A.tau_f[j * 3 * Kf + kf3]);
+            }
+        }
+        tau[i * 3 * Kc + kc3] = t;
     }
 }
 
@@ -429,9 +441,10 @@ void pair_restrict_states(pswe_pair* P, cudaStream_t st) {
     PSWE_LAUNCH_CHECK();
 }
 
-void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st) {
+void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st, const double2* tau_f) {
     pswe_level *F = P->fine, *C = P->coarse;
     FasArgs A{};
+    A.tau_f = tau_f;
     A.mc = C->nn;
     A.mf = F->nn;
     A.Rf = F->R;
@@ -447,6 +460,7 @@ void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st) {
     }
     for (int i = 0; i < C->nn; ++i) {
         for (int j = 0; j < F->nn; ++j) A.qfr[i][j] = P->qfr[(size_t)i * F->nn + j];
+        for (int j = 0; j < F->nn; ++j) A.tr[i][j] = P->tr[(size_t)i * F->nn + j];
         for (int j = 0; j < C->nn; ++j) A.qc[i][j] = C->tab.Q(i, j);
     }
     const long n = 3 * C->K;
@@ -715,7 +729,15 @@ int pswe_restrict_states(pswe_pair* P, void* stream) {
 int pswe_fas_correction(pswe_pair* P, double dt, double* tau, void* stream) {
     return guarded([&] {
         if (!P || !tau) throw std::invalid_argument("NULL argument");
-        pair_fas(P, dt, reinterpret_cast<double2*>(tau), as_stream(stream));
+        pair_fas(P, dt, reinterpret_cast<double2*>(tau), as_stream(stream), nullptr);
+    });
+}
+
+int pswe_fas_correction_ml(pswe_pair* P, double dt, const double* tau_fine, double* tau, void* stream) {
+    return guarded([&] {
+        if (!P || !tau) throw std::invalid_argument("NULL argument");
+        pair_fas(P, dt, reinterpret_cast<double2*>(tau), as_stream(stream),
+                 reinterpret_cast<const double2*>(tau_fine));
     });
 }
 

@@ -59,9 +59,15 @@ class TransferPair:
         """coarse.state := restrict_states(fine.state) (multilevel.cpp:100-107)."""
         _lib.check(_lib.lib().pswe_restrict_states(self._h, _stream()))
 
-    def fas_correction(self, dt: float):
-        """tau := fas_correction(fine, coarse, dt) (multilevel.cpp:109-137)."""
-        _lib.check(_lib.lib().pswe_fas_correction(self._h, float(dt), self.tau.data_ptr(), _stream()))
+    def fas_correction(self, dt: float, tau_fine=None):
+        """tau := fas_correction(fine, coarse, dt) (multilevel.cpp:109-137); with tau_fine (the fine
+        level's own FAS term, fine num_nodes states) the multi-level form of Eq. 19
+        (PAPER.md:576-581): tau += R tau_fine."""
+        if tau_fine is None:
+            _lib.check(_lib.lib().pswe_fas_correction(self._h, float(dt), self.tau.data_ptr(), _stream()))
+        else:
+            _lib.check(_lib.lib().pswe_fas_correction_ml(self._h, float(dt), tau_fine.data_ptr(),
+                                                         self.tau.data_ptr(), _stream()))
         return self.tau
 
     def save_coarse(self):

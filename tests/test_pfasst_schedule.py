@@ -36,6 +36,39 @@ def test_schedule_message_log_matches_reference(golden, n_ts):
     assert _log_from_schedule(P, n_ts, 3, 5, 3) == ref
 
 
+_LEVEL = {"SEND_FINE": 0, "RECV_FINE_IC": 0, "SEND_MID": 1, "RECV_MID_IC": 1}
+
+
+@pytest.mark.parametrize("n_levels", [2, 3])
+@pytest.mark.parametrize("n,n_iter", [(1, 1), (2, 3), (4, 3), (8, 4)])
+def test_schedule_queues_consistent(n_levels, n, n_iter):
+    """Replay every worker's schedule in worker order (the serial executor's order) through FIFO
+    queues per (receiver, level): each receive must find the message its sender tagged with the
+    same (phase, iteration) - the check the C++ executors make - and no message may be left over.
+    Covers the three-level V-cycle schedule (BASELINE config 4), which has no reference log."""
+    import collections
+
+    import paper_1904_05988_b200 as P
+    lc = n_levels - 1
+    level = dict(_LEVEL, SEND_COARSE=lc, RECV_COARSE_IC=lc)
+    q = collections.defaultdict(collections.deque)
+    counts = collections.Counter()
+    for w in range(n):
+        for op, phase, it, _ in P.schedule(w, n, n_iter, n_levels):
+            if op.startswith("SEND_"):
+                q[(w + 1, level[op])].append((phase, it))
+                counts[level[op]] += 1
+            elif op.startswith("RECV_"):
+                assert q[(w, level[op])], f"w={w} {op} on an empty channel"
+                assert q[(w, level[op])].popleft() == (phase, it), f"w={w} {op} tag mismatch"
+    assert all(len(v) == 0 for v in q.values())
+    # coarse: n(n-1)/2 predictor + (N-1)(n-1) iteration messages; fine and mid: (N-1)(n-1)
+    assert counts[lc] == n * (n - 1) // 2 + (n_iter - 1) * (n - 1)
+    assert counts[0] == (n_iter - 1) * (n - 1)
+    if n_levels == 3:
+        assert counts[1] == (n_iter - 1) * (n - 1)
+
+
 def test_schedule_counts():
     """coarse messages n(n-1)/2 + (N-1)(n-1), fine (N-1)(n-1)."""
     import paper_1904_05988_b200 as P
