@@ -19,7 +19,8 @@ Side results on the same JSON line:
   cpu_baseline   the reference (oracle/_ref, compiled from /root/reference) timed on the host
                  cores, rank 0 at N=1 only;
   pfasst         config-3 PFASST block (T255 256x512 / T127 128x256, 5/3 nodes, dt 60 s, 8 steps, 4 its),
-                 n_ts = N time ranks (NCCL) — wall s per simulated day;
+                 n_ts = N time ranks (NCCL) — wall s per simulated day; pfasst_configs adds
+                 config 4 (three-level T511/T255/T127) and config 5 (T1023/T511);
   transform      config-2 micro-bench: 15-field round trip at T255 on 256 x 512.
 --impl reference times the reference's CPU path (oracle/_ref) on the same workload.
 """
@@ -397,12 +398,14 @@ def run_ours(args):
                  "frac_of_fp64_peak": rt_flops / (tms * 1e-3) / 1e12 / peak}
 
     # PFASST (config-3 shape) at n_ts = world
-    pf_res = None
+    pf_res, pf_all = None, {}
     if not args.no_pfasst:
-        try:
-            pf_res = run_pfasst(P, prm, world, rank, dev, clocks_dev=local)
-        except Exception as e:  # reported, never hides the headline
-            pf_res = {"error": f"{type(e).__name__}: {e}"}
+        for c in (3, 4, 5):
+            try:
+                pf_all[str(c)] = run_pfasst(P, prm, world, rank, dev, clocks_dev=local, config=c)
+            except Exception as e:  # reported, never hides the headline
+                pf_all[str(c)] = {"error": f"{type(e).__name__}: {e}"}
+        pf_res = pf_all.get("3")
 
     clk = clocks.stop()
 
@@ -428,7 +431,7 @@ def run_ours(args):
                        "parallelism": f"{world} rank(s), independent states per rank"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": gpu_launches,
             "transform": transform, "pfasst": pf_res, "sequential_single_state": sequential,
-            "dealiased_grid": dealiased,
+            "dealiased_grid": dealiased, "pfasst_configs": pf_all,
         }
         print(json.dumps(line))
     if world > 1:
@@ -436,29 +439,41 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_pfasst(P, prm, world, rank, dev, clocks_dev=0):
-    """Config 3: T255 (256x512) / T127 (128x256), 5/3 nodes, dt 60 s, 8 steps, 4 iterations."""
+PF_CONFIGS = {
+    # BASELINE configs[2..4]: (levels (R, nlat, nlon, nodes) fine -> coarse, dt, steps, iterations)
+    3: ([(255, 256, 512, 5), (127, 128, 256, 3)], 60.0, 8, 4),
+    4: ([(511, 512, 1024, 5), (255, 256, 512, 3), (127, 128, 256, 2)], 30.0, 16, 4),
+    5: ([(1023, 1024, 2048, 5), (511, 512, 1024, 3)], 15.0, 8, 3),
+}
+
+
+def run_pfasst(P, prm, world, rank, dev, clocks_dev=0, config=3):
+    """PFASST blocks of a BASELINE config at n_ts = world time ranks (one per GPU, NCCL; serial
+    emulation of the one worker at world = 1): wall s per simulated day. Config 4 is three-level
+    (the reference has no three-level implementation; grids for the coarse levels: the linear
+    (R+1) x 2(R+1) grid, BASELINE states only the fine grid); config 4's iteration count is not
+    stated (4, as config 3)."""
     import torch
     import torch.distributed as dist
 
     from paper_1904_05988_b200.cases import config_state
-    steps, dt, n_iter = 8, 60.0, 4
+    lv, dt, steps, n_iter = PF_CONFIGS[config]
     if steps % world:
-        return {"skipped": f"8 steps not divisible by {world} ranks"}
+        return {"skipped": f"{steps} steps not divisible by {world} ranks"}
     n_blocks = steps // world
-    pf_plan = P.TransformPlan(255, 256, 512)
-    pc_plan = P.TransformPlan(127, 128, 256)
-    fine, coarse = P.Level(pf_plan, prm, 5), P.Level(pc_plan, prm, 3)
-    pair = P.TransferPair(fine, coarse)
+    plans = [P.TransformPlan(R, nlat, nlon) for R, nlat, nlon, _ in lv]
+    levels = [P.Level(pl, prm, nn) for pl, (_, _, _, nn) in zip(plans, lv)]
+    pair = P.TransferPair(levels[0], levels[1])
+    pair2 = P.TransferPair(levels[1], levels[2]) if len(levels) == 3 else None
     cfg = P.BlockConfig(world, dt, n_iter)
     if world == 1:
-        pf = P.Pfasst(pair, cfg)
+        pf = P.Pfasst(pair, cfg, pair2=pair2)
     else:
         uid = [P.pfasst.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        pf = P.Pfasst(pair, cfg, rank=rank, world=world, nccl_id=uid[0])
-    theta0 = torch.as_tensor(config_state(3, pf_plan)).to(dev)
-    P.run_blocks(pf, theta0, 1)  # warm-up block
+        pf = P.Pfasst(pair, cfg, rank=rank, world=world, nccl_id=uid[0], pair2=pair2)
+    theta0 = torch.as_tensor(config_state(config, plans[0])).to(dev)
+    P.run_blocks(pf, theta0, 1)  # warm-up block (also captures the serial-emulation graph)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -473,8 +488,12 @@ def run_pfasst(P, prm, world, rank, dev, clocks_dev=0):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     wall = ms * 1e-3
-    return {"config": "config 3: T255(256x512)/T127(128x256), 5/3 nodes, dt 60 s, 8 steps, 4 iterations",
-            "n_ts": world, "blocks": n_blocks, "wall_s": wall, "wall_s_per_sim_day": wall / (steps * dt) * 86400,
+    desc = "/".join(f"T{R}({nlat}x{nlon})" for R, nlat, nlon, _ in lv)
+    nodes = "/".join(str(nn) for *_, nn in lv)
+    pf.close()
+    return {"config": f"config {config}: {desc}, {nodes} nodes, dt {dt:g} s, {steps} steps, {n_iter} iterations",
+            "levels": len(lv), "n_ts": world, "blocks": n_blocks, "wall_s": wall,
+            "wall_s_per_sim_day": wall / (steps * dt) * 86400,
             "final_residuals": [float(r) for r in hist[-1][:, -1]]}
 
 

@@ -6,9 +6,14 @@ its analytic cases live in proj/src/cases.cpp:43-167 and are not used by BASELIN
   linear balance  lap(Phi') = div(f grad psi), f = 2 Omega mu;  Phi(0,0) = phi_bar sqrt(2)
   (P^0_0 = 1/sqrt(2), test_transform.cpp:60-61).
 * ``add_gaussian_bump``: + g * A exp(-(d/r)^2) at a seeded centre (config 3).
+* ``add_zonal_jet``: + u = u0 sin^2(2 phi) in the northern hemisphere (config 4), vorticity and
+  divergence by the GPU vortdiv_from_uv, geopotential in gradient-wind balance
+  dPhi/dphi = -a u (2 Omega sin phi + u tan phi / a), integrated in latitude with the global mean
+  removed (the mean geopotential stays phi_bar).
 
-Host numpy does only coefficient set-up (random draws, spectral scalings); the one grid
-operation (the bump's analysis) runs on the GPU through TransformPlan.analyse.
+Host numpy does only coefficient set-up (random draws, spectral scalings) and 1-D latitude
+profiles; the grid operations (the bump's and the jet's analysis) run on the GPU through
+TransformPlan.
 
 Conventions:
 * the rms velocity is the spectral (continuous) one, mean |V|^2 = 1/2 sum' s(s+1)/a^2 |psi_rs|^2
@@ -101,8 +106,37 @@ def add_gaussian_bump(state: np.ndarray, plan: TransformPlan, amplitude_m: float
     return out
 
 
+def add_zonal_jet(state: np.ndarray, plan: TransformPlan, u0: float = 60.0, radius: float = 6.37122e6,
+                  omega: float = 7.292e-5) -> np.ndarray:
+    lat = np.arcsin(plan.mu)
+
+    def u_of(phi):
+        return np.where(phi > 0.0, u0 * np.sin(2.0 * phi) ** 2, 0.0)
+
+    # gradient-wind balance integrated on a fine latitude grid (u = 0 south of the equator)
+    fine = np.linspace(0.0, 0.5 * math.pi, 20001)
+    uf = u_of(fine)
+    with np.errstate(invalid="ignore"):
+        dphi = -radius * uf * (2.0 * omega * np.sin(fine) + uf * np.tan(fine) / radius)
+    dphi[-1] = 0.0  # u = 0 at the pole
+    prof = np.concatenate([[0.0], np.cumsum(0.5 * (dphi[1:] + dphi[:-1]) * np.diff(fine))])
+    geo = np.interp(np.maximum(lat, 0.0), fine, prof)
+    geo -= 0.5 * float(np.sum(plan.weight * geo))  # zero global mean (Gauss weights sum to 2)
+    ug = np.repeat(u_of(lat)[:, None], plan.nlon, axis=1)
+    u = torch.as_tensor(ug).cuda()
+    zeta, delta = plan.vortdiv_from_uv(u, torch.zeros_like(u), radius)
+    phi_c = plan.analyse(torch.as_tensor(np.repeat(geo[:, None], plan.nlon, axis=1)).cuda())
+    out = state.copy()
+    out[0] += phi_c.cpu().numpy()
+    out[1] += zeta.cpu().numpy()
+    out[2] += delta.cpu().numpy()
+    return out
+
+
 def config_state(config: int, plan: TransformPlan | None = None, seed: int = 1904_05988) -> np.ndarray:
-    """BASELINE.json configs: 1 (T63, 20 m/s), 3 (T255, 40 m/s + bump), 5 (T1023, 30 m/s)."""
+    """BASELINE.json configs: 1 (T63, 20 m/s), 3 (T255, 40 m/s + bump), 4 (T511, 20 m/s + zonal
+    jet; the rms wind of config 4's random field is not stated, 20 m/s as config 1), 5 (T1023,
+    30 m/s)."""
     phi_bar = 9.80616 * 1e4
     if config == 1:
         return balanced_random_state(63, 20.0, seed, phi_bar=phi_bar)
@@ -111,6 +145,11 @@ def config_state(config: int, plan: TransformPlan | None = None, seed: int = 190
         if plan is not None:
             s = add_gaussian_bump(s, plan, 120.0, 5.0e5, seed + 1)
         return s
+    if config == 4:
+        s = balanced_random_state(511 if plan is None else plan.R, 20.0, seed, phi_bar=phi_bar)
+        if plan is not None:
+            s = add_zonal_jet(s, plan)
+        return s
     if config == 5:
         return balanced_random_state(1023, 30.0, seed, phi_bar=phi_bar)
-    raise ValueError("config must be 1, 3 or 5")
+    raise ValueError("config must be 1, 3, 4 or 5")

@@ -137,3 +137,26 @@ def test_implicit_solve_residual(P):
     b[1, O.index(R, 0, 2)] = 1.0
     x = host(P.solve_implicit(R, cuda(b), 1.0, p))
     assert abs(x[1, O.index(R, 0, 2)].real - 1.0 / 7.0) < 1e-15
+
+
+def test_zonal_jet_is_balanced(P):
+    """config 4's jet (cases.add_zonal_jet): a zonal flow in gradient-wind balance is a steady
+    state of the nonlinear SWE, so its tendencies are small next to the same jet without the
+    balancing geopotential."""
+    from paper_1904_05988_b200.cases import add_zonal_jet
+    R = 85
+    plan = P.TransformPlan(R, 128, 256)
+    p = P.ModelParams(phi_bar=9.80616 * 1e4)
+    base = np.zeros((3, P.num_coeffs(R)), dtype=np.complex128)
+    base[0, 0] = p.phi_bar * math.sqrt(2.0)
+    jet = add_zonal_jet(base, plan)
+    unbal = jet.copy()
+    unbal[0] = base[0]
+    def tendency(st):  # F_I + F_E: the balance is a cancellation between the two parts
+        fi, fe = P.imex_split(cuda(st), p, plan)
+        return np.abs(host(fi) + host(fe)).max(axis=1)
+
+    t_bal, t_unb = tendency(jet), tendency(unbal)
+    # Phi and zeta tendencies vanish for any zonal flow; the divergence tendency is the balance
+    assert t_bal[2] < 3e-2 * t_unb[2]
+    assert t_bal[0] < 1e-6 * p.phi_bar and t_bal[1] < 1e-12
