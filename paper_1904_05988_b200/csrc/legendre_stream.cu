@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
 // bulk copy of the G tile of each order (both hemispheres, written in this layout by the grid
 // stage) and one 1 KB copy per chunk of the P table, into an S-stage mbarrier ring.
 // G_E = G_N + G_S and G_O = G_N - G_S are formed in registers and reused by the CPW chunks.
-template <int NTC, int W, int CPW, int S>
+template <int NTC, int W, int CPW, int S, int SUB>
 __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int nq, GtLayout gl,
                                                            const double* __restrict__ ptab,
                                                            const int* __restrict__ cbase,
@@ -243,10 +243,12 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
     __shared__ long pbase[NS];
     __shared__ int pslot[NS], npc;
     const int sgc = gl.sgc;
-    const int gstage = 2 * 8 * sgc;              // doubles of one order's G stage
-    double* sG = smem;                           // [S][2 orders][2][8][sgc]
-    double* sP = sG + S * 2 * gstage;            // [S][NS][8 * 16]
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(sP + S * NS * 128);
+    const int gsub = 2 * 8 * sgc;                // doubles of one 8-latitude sub-stage of G
+    const int gstage = SUB * gsub;               // doubles of one order's G stage
+    constexpr int PS = SUB * 128;                // doubles of one chunk's P stage
+    double* sG = smem;                           // [S][2 orders][SUB][2][8][sgc]
+    double* sP = sG + S * 2 * gstage;            // [S][NS][SUB * 8 * 16]
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(sP + S * NS * PS);
     unsigned long long* empty = full + S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int4 ta = tasks_a[blockIdx.x];
@@ -255,13 +257,14 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
     const int wa = (na + CPW - 1) / CPW;  // warps of order a
     const int z = blockIdx.y;
     const int ns8 = gl.ns8;
+    const int nst = ns8 / SUB;  // stages of 8 SUB latitudes
     const bool ord_b = warp >= wa;
     const int my_m = ord_b ? ta.w : ta.x;
     const int my_c0 = ord_b ? tb.x + (warp - wa) * CPW : ta.y + warp * CPW;
     const int my_n = max(0, min(CPW, ord_b ? nb - (warp - wa) * CPW : na - warp * CPW));
     const bool mine = my_n > 0;
-    const double* __restrict__ ga = gt + ((long)z * (R + 1) + ta.x) * ns8 * gstage;
-    const double* __restrict__ gb = gt + ((long)z * (R + 1) + ta.w) * ns8 * gstage;
+    const double* __restrict__ ga = gt + ((long)z * (R + 1) + ta.x) * ns8 * gsub;
+    const double* __restrict__ gb = gt + ((long)z * (R + 1) + ta.w) * ns8 * gsub;
     const int r4 = lane >> 2, c4 = lane & 3;
     const unsigned GB = (unsigned)gstage * sizeof(double);
 
@@ -289,16 +292,17 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
     pdl_trigger();
     pdl_wait();  // G tiles come from the grid stage
     const int np = npc;
-    auto issue = [&](int s8) {
-        const int k = s8 % S;
-        mbar_expect_tx(full + k, GB * (nb > 0 ? 2u : 1u) + np * 1024u);
-        bulk_g2s(sG + (k * 2) * gstage, ga + (long)s8 * gstage, GB, full + k);
-        if (nb > 0) bulk_g2s(sG + (k * 2 + 1) * gstage, gb + (long)s8 * gstage, GB, full + k);
-        const long ps = (s8 >> 2) * 512 + (s8 & 3) * 128;
-        for (int u = 0; u < np; ++u) bulk_g2s(sP + (k * NS + pslot[u]) * 128, ptab + pbase[u] + ps, 1024u, full + k);
+    auto issue = [&](int q) {  // stage q: latitude rows 8 SUB q .. 8 SUB q + 8 SUB - 1
+        const int k = q % S;
+        constexpr unsigned PB = PS * sizeof(double);
+        mbar_expect_tx(full + k, GB * (nb > 0 ? 2u : 1u) + np * PB);
+        bulk_g2s(sG + (k * 2) * gstage, ga + (long)q * gstage, GB, full + k);
+        if (nb > 0) bulk_g2s(sG + (k * 2 + 1) * gstage, gb + (long)q * gstage, GB, full + k);
+        const long ps = (long)q * PS;  // P tile rows are contiguous within a 32-latitude slice
+        for (int u = 0; u < np; ++u) bulk_g2s(sP + (k * NS + pslot[u]) * PS, ptab + pbase[u] + ps, PB, full + k);
     };
     if (threadIdx.x == 0)
-        for (int s8 = 0; s8 < S && s8 < ns8; ++s8) issue(s8);
+        for (int q = 0; q < S && q < nst; ++q) issue(q);
 
     double acc[NTC][CPW][2][2];
 #pragma unroll
@@ -306,14 +310,16 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
 #pragma unroll
         for (int b = 0; b < CPW; ++b) acc[a][b][0][0] = acc[a][b][0][1] = acc[a][b][1][0] = acc[a][b][1][1] = 0.0;
 
-    for (int s8 = 0; s8 < ns8; ++s8) {
-        const int k = s8 % S;
-        const unsigned ph = (unsigned)(s8 / S) & 1u;
+    for (int q = 0; q < nst; ++q) {
+        const int k = q % S;
+        const unsigned ph = (unsigned)(q / S) & 1u;
         mbar_wait(full + k, ph);
         __syncwarp();
         if (mine) {
-            const double* g = sG + (k * 2 + (ord_b ? 1 : 0)) * gstage;
-            const double* pt = sP + (k * NS + warp * CPW) * 128;
+#pragma unroll
+            for (int sub = 0; sub < SUB; ++sub) {
+            const double* g = sG + (k * 2 + (ord_b ? 1 : 0)) * gstage + sub * gsub;
+            const double* pt = sP + (k * NS + warp * CPW) * PS + sub * 128;
 #pragma unroll
             for (int ks = 0; ks < 2; ++ks) {
                 const int rr = 4 * ks + c4;  // latitude row of this lane's k
@@ -328,8 +334,8 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
                 }
 #pragma unroll
                 for (int cc = 0; cc < CPW; ++cc) {
-                    be[cc] = pt[cc * 128 + rr * 16 + pswz(c4, r4)];
-                    bo[cc] = pt[cc * 128 + rr * 16 + pswz(c4, 8 + r4)];
+                    be[cc] = pt[cc * PS + rr * 16 + pswz(c4, r4)];
+                    bo[cc] = pt[cc * PS + rr * 16 + pswz(c4, 8 + r4)];
                 }
 #pragma unroll
                 for (int nt = 0; nt < NTC; ++nt)
@@ -339,12 +345,13 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
                         dmma(acc[nt][cc][1], ao[nt], bo[cc]);
                     }
             }
+            }  // sub-stages
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + k);
-        if (threadIdx.x == 0 && s8 + S < ns8) {
+        if (threadIdx.x == 0 && q + S < nst) {
             mbar_wait(empty + k, ph);
-            issue(s8 + S);
+            issue(q + S);
         }
     }
     if (!mine) return;
@@ -373,12 +380,12 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
     }
 }
 
-template <int NTC, int W, int CPW, int S>
+template <int NTC, int W, int CPW, int S, int SUB = 1>
 void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out, cudaStream_t st) {
     const int Jp = ((P.J + 31) / 32) * 32;
-    const size_t sm = (size_t)S * (2 * 2 * 8 * gl.sgc + W * CPW * 128) * sizeof(double) +
+    const size_t sm = (size_t)S * SUB * (2 * 2 * 8 * gl.sgc + W * CPW * 128) * sizeof(double) +
                       2 * S * sizeof(unsigned long long);
-    auto kern = leg_fwd_gt_kernel<NTC, W, CPW, S>;
+    auto kern = leg_fwd_gt_kernel<NTC, W, CPW, S, SUB>;
     static int attr = 0;
     if ((int)sm > attr) {
         PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -671,7 +678,13 @@ void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t s
     }
     static_assert(kFwdCfg[0].warps == 8 && kFwdCfg[0].cpw == 1 && kFwdCfg[0].stages == 4, "cfg 0");
     static_assert(kFwdCfg[1].warps == 4 && kFwdCfg[1].cpw == 2 && kFwdCfg[1].stages == 3, "cfg 1");
-    if (P.fwd_cfg == 0) {
+    if (P.fwd_cfg == 0 && gl.ntc <= 3) {
+        // one or two states: stages of 32 latitudes (four 8-latitude sub-stages per bulk copy, whole
+        // 4 KB P tiles) - the per-stage work of narrow column groups is too short to amortise one
+        // bulk-copy round trip per 8 latitudes
+        if (gl.ntc == 2) fwd_gt_launch<2, 8, 1, 2, 4>(P, gl, 5 * n, out, st);
+        else fwd_gt_launch<3, 8, 1, 2, 4>(P, gl, 5 * n, out, st);
+    } else if (P.fwd_cfg == 0) {
         PSWE_FWD_CASES(8, 1, 4)
     } else {
         PSWE_FWD_CASES(4, 2, 3)
