@@ -685,7 +685,13 @@ void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t s
         if (gl.ntc == 2) fwd_gt_launch<2, 8, 1, 2, 4>(P, gl, 5 * n, out, st);
         else fwd_gt_launch<3, 8, 1, 2, 4>(P, gl, 5 * n, out, st);
     } else if (P.fwd_cfg == 0) {
-        PSWE_FWD_CASES(8, 1, 4)
+        // wider groups: 16-latitude stages in a 2-deep ring (measured faster than 8-latitude stages
+        // in a 4-deep ring: half the bulk copies; T255 384x768 forward 48.7 -> 43.5 us)
+        switch (gl.ntc) {
+            case 4: fwd_gt_launch<4, 8, 1, 2, 2>(P, gl, 5 * n, out, st); break;
+            case 5: fwd_gt_launch<5, 8, 1, 2, 2>(P, gl, 5 * n, out, st); break;
+            default: fwd_gt_launch<7, 8, 1, 2, 2>(P, gl, 5 * n, out, st); break;
+        }
     } else {
         PSWE_FWD_CASES(4, 2, 3)
     }
