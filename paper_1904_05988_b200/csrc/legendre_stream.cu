@@ -3,13 +3,14 @@
 // arrive by cp.async instead of being recomputed, which removes the serial recurrence chains
 // and the checkpoint loads from the contraction kernels.
 //
-// Table layout (built once per plan by the same recurrence, legendre.cpp:30-37):
-//   ptab[(cbase(m) + c) * Jp * 16 + j * 16 + (col ^ ((j & 3) << 2))] = P^m_{m + 16c + tl}(mu_j),
+// Table layout (built once per plan by the same recurrence, legendre.cpp:30-37): per m, per
+// 32-latitude slice sl, per 16-degree chunk c, a 4 KB tile [32 rows][16] (ptile_off),
+//   tile[row * 16 + (col ^ ((row & 3) << 2))] = P^m_{m + 16c + tl}(mu_{32 sl + row}),
 //   col = (tl & 1) * 8 + (tl >> 1)
-// i.e. per m, per 16-degree chunk c, per latitude j: the 8 even then the 8 odd degrees, XOR-
-// swizzled within the row. A (chunk, 32-latitude slice) tile is one contiguous 4 KB block that is
-// exactly its shared-memory image: one bulk copy, and both fragment patterns below read it in two
-// conflict-free wavefronts. Degrees past R+1 are zero.
+// i.e. the 8 even then the 8 odd degrees of a latitude, XOR-swizzled within the row. A tile is
+// exactly its shared-memory image (one bulk copy; both fragment patterns below read it in two
+// conflict-free wavefronts), and the chunks of one slice are contiguous, so a run of chunks is one
+// copy. Degrees past R+1 are zero.
 //
 // forward  Y^T[col][t] = sum_j G_par^T[col][j] P[j][t]:  A = G^T (smem, swizzled), B = P tile
 // inverse  E/O[j][col]  = sum_t P[j][t] X[t][col]:         A = P tile, B = X tile (smem)
@@ -32,6 +33,11 @@ using legc::dmma;
 
 // swizzled column of degree-slot col (0..15) in latitude row j of a P tile
 __host__ __device__ __forceinline__ int pswz(int j, int col) { return col ^ ((j & 3) << 2); }
+// doubles offset of tile (chunk c, 32-latitude slice sl) of the order whose chunk base is cbm
+// and chunk count nch; nsl slices per order
+__host__ __device__ __forceinline__ long ptile_off(int cbm, int nch, int nsl, int c, int sl) {
+    return ((long)cbm * nsl + (long)sl * nch + c) * 512;
+}
 
 __device__ __forceinline__ double rec_step(double2 ab, double mu, double p, double pm1) {
     return __fma_rn(ab.x, __dmul_rn(mu, p), -__dmul_rn(ab.y, pm1));
@@ -97,10 +103,11 @@ __global__ void build_ptab2_kernel(int R, int J, int Jp, const double* __restric
     if (j >= Jp) return;
     const int len = R + 2 - m;
     const int nch = (len + CH - 1) / CH;
-    double* out = ptab + (long)cbase[m] * Jp * 16 + (long)j * 16;
+    const int nsl = Jp >> 5, row = j & 31;
+    double* out = ptab + ptile_off(cbase[m], nch, nsl, 0, j >> 5) + row * 16;  // chunk c: + c * 512
     if (j >= J) {
         for (int c = 0; c < nch; ++c)
-            for (int i = 0; i < 16; ++i) out[(long)c * Jp * 16 + i] = 0.0;
+            for (int i = 0; i < 16; ++i) out[(long)c * 512 + i] = 0.0;
         return;
     }
     const double mu = mu_n[j];
@@ -108,7 +115,7 @@ __global__ void build_ptab2_kernel(int R, int J, int Jp, const double* __restric
     double p = seed[(long)m * J + j], pm1 = 0.0;
     for (int t = 0; t < nch * CH; ++t) {
         const int c = t / CH, tl = t % CH;
-        out[(long)c * Jp * 16 + pswz(j, (tl & 1) * 8 + (tl >> 1))] = t < len ? p : 0.0;
+        out[(long)c * 512 + pswz(row, (tl & 1) * 8 + (tl >> 1))] = t < len ? p : 0.0;
         if (t < len) {
             const double pn = rec_step(__ldg(rc + t), mu, p, pm1);
             pm1 = p;
@@ -146,11 +153,11 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
     const int tmax = ext ? len : len - 1;
     const long bx = off_ext(R, m);
     const long Kx = (long)(R + 1) * (R + 4) / 2, K = (long)(R + 1) * (R + 2) / 2;
-    const double* __restrict__ pm = ptab + (long)cbase[m] * Jp * 16;
+    const double* __restrict__ pm = ptab + ptile_off(cbase[m], nch, nsl, 0, 0);  // + (sl nch + c) 512
 
     // first P tile of this warp's first chunk streams in while G is staged
     if (warp < nch) {
-        load_tile(tiles, pm + (long)warp * Jp * 16, lane);
+        load_tile(tiles, pm + (long)warp * 512, lane);
         cp_async_commit();
     }
 #ifndef PSWE_FDIAG_NOSTAGE
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
         for (int a = 0; a < 2; ++a)
 #pragma unroll
             for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-        const double* src = pm + (long)c * Jp * 16;
+        const double* src = pm + (long)c * 512;  // slice sl: + sl nch 512
 #ifndef PSWE_FDIAG_NOTILE
         if (!first) {  // the first task's tile was issued before the G staging
             load_tile(tiles, src, lane);
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
         first = false;
         for (int sl = 0; sl < nsl; ++sl) {
 #ifndef PSWE_FDIAG_NOTILE
-            if (sl + 1 < nsl) load_tile(tiles + ((sl + 1) & 1) * 32 * 16, src + (long)(sl + 1) * 32 * 16, lane);
+            if (sl + 1 < nsl) load_tile(tiles + ((sl + 1) & 1) * 32 * 16, src + (long)(sl + 1) * nch * 512, lane);
 #endif
             cp_async_commit();
             cp_async_wait<1>();
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
                                                            double2* __restrict__ out) {
     constexpr int NS = W * CPW;  // chunk slots
     extern __shared__ __align__(128) double smem[];
-    __shared__ long pbase[NS];
+    __shared__ long pbase[NS], pstride[NS];  // tile (chunk, slice 0) offset; per-slice stride
     __shared__ int pslot[NS], npc;
     const int sgc = gl.sgc;
     const int gsub = 2 * 8 * sgc;                // doubles of one 8-latitude sub-stage of G
@@ -276,7 +283,9 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
             const int c0 = b ? tb.x + (w - wa) * CPW : ta.y + w * CPW;
             const int nn = max(0, min(CPW, b ? nb - (w - wa) * CPW : na - w * CPW));
             for (int u = 0; u < nn; ++u) {
-                pbase[n] = (long)(cbase[m] + c0 + u) * Jp * 16;
+                const int nchm = (R + 2 - m + CH - 1) / CH;
+                pbase[n] = ptile_off(cbase[m], nchm, Jp >> 5, c0 + u, 0);
+                pstride[n] = (long)nchm * 512;
                 pslot[n] = w * CPW + u;
                 ++n;
             }
@@ -298,8 +307,10 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
         mbar_expect_tx(full + k, GB * (nb > 0 ? 2u : 1u) + np * PB);
         bulk_g2s(sG + (k * 2) * gstage, ga + (long)q * gstage, GB, full + k);
         if (nb > 0) bulk_g2s(sG + (k * 2 + 1) * gstage, gb + (long)q * gstage, GB, full + k);
-        const long ps = (long)q * PS;  // P tile rows are contiguous within a 32-latitude slice
-        for (int u = 0; u < np; ++u) bulk_g2s(sP + (k * NS + pslot[u]) * PS, ptab + pbase[u] + ps, PB, full + k);
+        const int sub0 = q * SUB;  // first 8-latitude sub-slice: rows of slice sub0 / 4
+        for (int u = 0; u < np; ++u)
+            bulk_g2s(sP + (k * NS + pslot[u]) * PS, ptab + pbase[u] + (sub0 >> 2) * pstride[u] + (sub0 & 3) * 128,
+                     PB, full + k);
     };
     if (threadIdx.x == 0)
         for (int q = 0; q < S && q < nst; ++q) issue(q);
@@ -505,7 +516,7 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
     const int nact = min(WS, nsl - sl0);
     const int z = blockIdx.z;
     const int q0 = z * 4 * NT;
-    const double* __restrict__ pm = ptab + (long)cbase[m] * Jp * 16 + (long)sl0 * 512;
+    const double* __restrict__ pm = ptab + ptile_off(cbase[m], nch, nsl, 0, sl0);  // slice sl0 + w: + w nch 512
     const double* __restrict__ xm = Xt + ((long)z * nct + cbase[m]) * CH * SX;
     const int r4 = lane >> 2, c4 = lane & 3;
 
@@ -523,7 +534,7 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
         const int k = c % S;
         mbar_expect_tx(full + k, nact * PB + XB);
         for (int w = 0; w < nact; ++w)
-            bulk_g2s(sP + (k * WS + w) * 512, pm + (long)c * Jp * 16 + w * 512, PB, full + k);
+            bulk_g2s(sP + (k * WS + w) * 512, pm + ((long)w * nch + c) * 512, PB, full + k);
         bulk_g2s(sX + k * CH * SX, xm + (long)c * CH * SX, XB, full + k);
     };
 #ifndef PSWE_DIAG_NOTMA
