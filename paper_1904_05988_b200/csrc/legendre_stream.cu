@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(CH * kPrepItems)
 // warps); the P and X tiles of a stage are shared by all warps of the block. An S-stage ring of
 // {WS P tiles, one X tile} per chunk is filled by bulk copies from thread 0 (full[s]: expect_tx +
 // complete_tx) and released by one arrival per warp (empty[s]).
-template <int NT, int S, int WS>
+template <int NT, int S, int WS, int CPS>
 __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int Jp, int nlat, int nq, int nct,
                                                              const double* __restrict__ ptab,
                                                              const int* __restrict__ cbase,
@@ -502,9 +502,9 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
     constexpr unsigned PB = 32 * 16 * sizeof(double);
     constexpr unsigned XB = CH * SX * sizeof(double);
     extern __shared__ __align__(128) double smem[];
-    double* sP = smem;                 // [S][WS][32 * 16]
-    double* sX = sP + S * WS * 512;    // [S][CH * SX]
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(sX + S * CH * SX);
+    double* sP = smem;                      // [S][WS][CPS][32 * 16]
+    double* sX = sP + S * WS * CPS * 512;   // [S][CPS][CH * SX]
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(sX + S * CPS * CH * SX);
     unsigned long long* empty = full + S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ws = warp >> 1, mh = warp & 1;
@@ -530,16 +530,17 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
     __syncthreads();
     pdl_trigger();
     pdl_wait();  // X tiles come from the prep kernel
-    auto issue = [&](int c) {
-        const int k = c % S;
-        mbar_expect_tx(full + k, nact * PB + XB);
+    const int ngr = (nch + CPS - 1) / CPS;  // stages of CPS chunks: one copy per slice, one X copy
+    auto issue = [&](int g) {
+        const int k = g % S, c0 = g * CPS, nc = min(CPS, nch - c0);
+        mbar_expect_tx(full + k, nc * (nact * PB + XB));
         for (int w = 0; w < nact; ++w)
-            bulk_g2s(sP + (k * WS + w) * 512, pm + ((long)w * nch + c) * 512, PB, full + k);
-        bulk_g2s(sX + k * CH * SX, xm + (long)c * CH * SX, XB, full + k);
+            bulk_g2s(sP + (k * WS + w) * CPS * 512, pm + ((long)w * nch + c0) * 512, nc * PB, full + k);
+        bulk_g2s(sX + k * CPS * CH * SX, xm + (long)c0 * CH * SX, nc * XB, full + k);
     };
 #ifndef PSWE_DIAG_NOTMA
     if (threadIdx.x == 0)
-        for (int c = 0; c < S && c < nch; ++c) issue(c);
+        for (int g = 0; g < S && g < ngr; ++g) issue(g);
 #endif
 
     double acc[2][2][NT][2];  // [m-tile 2 mh + a][parity][n-tile][v]
@@ -550,16 +551,19 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
 #pragma unroll
             for (int cc = 0; cc < NT; ++cc) acc[a][b][cc][0] = acc[a][b][cc][1] = 0.0;
 
-    for (int c = 0; c < nch; ++c) {
-        const int k = c % S;
-        const unsigned ph = (unsigned)(c / S) & 1u;
+    for (int g = 0; g < ngr; ++g) {
+        const int k = g % S;
+        const unsigned ph = (unsigned)(g / S) & 1u;
+        const int nc = min(CPS, nch - g * CPS);
 #ifndef PSWE_DIAG_NOTMA
         mbar_wait(full + k, ph);
 #endif
         __syncwarp();
-        if (ws < nact) {
-            const double* tl = sP + (k * WS + ws) * 512 + mh * 16 * 16;  // this warp's 16 latitude rows
-            const double* xb = sX + k * CH * SX;
+#pragma unroll
+        for (int cc = 0; cc < CPS; ++cc)
+        if (ws < nact && cc < nc) {
+            const double* tl = sP + ((k * WS + ws) * CPS + cc) * 512 + mh * 16 * 16;  // this warp's 16 rows
+            const double* xb = sX + (k * CPS + cc) * CH * SX;
 #pragma unroll
             for (int par = 0; par < 2; ++par) {
 #pragma unroll
@@ -586,9 +590,9 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
         __syncwarp();
 #ifndef PSWE_DIAG_NOTMA
         if (lane == 0) mbar_arrive(empty + k);
-        if (threadIdx.x == 0 && c + S < nch) {
+        if (threadIdx.x == 0 && g + S < ngr) {
             mbar_wait(empty + k, ph);
-            issue(c + S);
+            issue(g + S);
         }
 #endif
     }
@@ -654,14 +658,27 @@ int inv_choose_nt(const pswe_plan& P, int nq) {
     return P.J >= 192 ? 3 : 2;
 }
 
+#ifndef PSWE_INV_CPS1
+#define PSWE_INV_CPS1 4
+#endif
+#ifndef PSWE_INV_CPS2
+#define PSWE_INV_CPS2 2
+#endif
+#ifndef PSWE_INV_CPS3
+#define PSWE_INV_CPS3 1
+#endif
 template <int NT>
 void inv_tma_launch(const pswe_plan& P, const double* Xt, int nq, double2* out, cudaStream_t st) {
-    constexpr int S = kInvStages, WS = kInvSlices;
+    // chunks per ring stage and ring depth by column-tile count (narrow groups do little DMMA work
+    // per chunk, so one stage carries several chunks: fewer bulk copies per DMMA)
+    constexpr int CPS = NT == 1 ? PSWE_INV_CPS1 : (NT == 2 ? PSWE_INV_CPS2 : PSWE_INV_CPS3);
+    constexpr int S = CPS == 1 ? kInvStages : (CPS == 2 ? 3 : 2), WS = kInvSlices;
     const int nsl = (P.J + 31) / 32;
     const int Jp = nsl * 32;
     const int groups = (nq + 4 * NT - 1) / (4 * NT);
-    const size_t sm = (size_t)S * (WS * 512 + CH * (8 * NT + 2)) * sizeof(double) + 2 * S * sizeof(unsigned long long);
-    auto kern = leg_inv_tma_kernel<NT, S, WS>;
+    const size_t sm = (size_t)S * CPS * (WS * 512 + CH * (8 * NT + 2)) * sizeof(double) +
+                      2 * S * sizeof(unsigned long long);
+    auto kern = leg_inv_tma_kernel<NT, S, WS, CPS>;
     static bool attr = false;
     if (!attr) {
         PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

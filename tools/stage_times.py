@@ -1,6 +1,6 @@
 """Per-kernel device times of one eval_imex call (CUDA events between the launches) for a few
 truncations and batch sizes. Usage: python tools/stage_times.py [R:nlat:nlon ...] (nlat 0 = default
-grid); with sizes given only those run, at batch 5."""
+grid); with sizes given only those run, at batch 5 (STAGE_BATCHES=1,5 to change)."""
 import ctypes
 import os
 import sys
@@ -21,7 +21,7 @@ SIZES = ((63, 0, 0), (127, 0, 0), (255, 0, 0), (255, 256, 512), (511, 0, 0), (10
 BATCHES = (1, 5)
 if len(sys.argv) > 1:
     SIZES = [tuple(int(x) for x in a.split(':')) for a in sys.argv[1:]]
-    BATCHES = (5,)
+    BATCHES = tuple(int(b) for b in os.environ.get("STAGE_BATCHES", "5").split(","))
 for R, nlat, nlon in SIZES:
     plan = P.TransformPlan(R, nlat, nlon, int(os.environ.get('LEGENDRE_MODE', '0')))
     for n in BATCHES:
