@@ -461,10 +461,34 @@ __global__ void __launch_bounds__(CH * kPrepItems)
                 vort = in + (long)item * K;
                 div = in2 + (long)item * K;
             }
-            const double2 chi = legc::inv_lap_at(div, bs, m, R, s, a2, rtab);
-            const double2 cpsi = legc::hcoef(vort, eps, bs, bx, m, R, s, a2, rtab);
-            const double2 psi = legc::inv_lap_at(vort, bs, m, R, s, a2, rtab);
-            const double2 cchi = legc::hcoef(div, eps, bs, bx, m, R, s, a2, rtab);
+            // the same values as legc::inv_lap_at / hcoef, with every load issued up front (clamped
+            // indices, range conditions applied afterwards) so they overlap in one memory round trip
+            const int sm1 = max(s - 1, m), sp1 = min(s + 1, R), s0 = min(s, R);
+            const double2 vm = vort[bs + sm1 - m], v0 = vort[bs + s0 - m], vp = vort[bs + sp1 - m];
+            const double2 dm = div[bs + sm1 - m], d0 = div[bs + s0 - m], dp = div[bs + sp1 - m];
+            const double rm = __ldg(rtab + max(s - 1, 0)), r0 = __ldg(rtab + s0), rp = __ldg(rtab + min(s + 1, R));
+            const double em = eps[bx + t], ep = eps[bx + min(t + 1, R + 1 - m)];  // stay inside block m
+            // inverse Laplacian factors -a^2/(s'(s'+1)) at s-1, s, s+1 (0 outside m..R and at 0)
+            const double fm = (s - 1 >= m && s - 1 >= 1) ? -a2 * rm : 0.0;
+            const double f0 = (s <= R && s >= 1) ? -a2 * r0 : 0.0;
+            const double fp = (s + 1 <= R) ? -a2 * rp : 0.0;
+            const double hm = (s - 1 >= m) ? -(double)(s - 1) * em : 0.0;  // H-sum weights
+            const double hp = (s + 1 <= R) ? (double)(s + 2) * ep : 0.0;
+            const double2 chi = make_double2(d0.x * f0, d0.y * f0);
+            const double2 psi = make_double2(v0.x * f0, v0.y * f0);
+            double2 cpsi = make_double2(0.0, 0.0), cchi = make_double2(0.0, 0.0);
+            if (s - 1 >= m) {
+                cpsi.x += hm * (vm.x * fm);
+                cpsi.y += hm * (vm.y * fm);
+                cchi.x += hm * (dm.x * fm);
+                cchi.y += hm * (dm.y * fm);
+            }
+            if (s + 1 <= R) {
+                cpsi.x += hp * (vp.x * fp);
+                cpsi.y += hp * (vp.y * fp);
+                cchi.x += hp * (dp.x * fp);
+                cchi.y += hp * (dp.y * fp);
+            }
             v[o] = make_double2(inv_a * (-m * chi.y - cpsi.x), inv_a * (m * chi.x - cpsi.y));
             v[o + 1] = make_double2(inv_a * (-m * psi.y + cchi.x), inv_a * (m * psi.x + cchi.y));
         }
