@@ -21,15 +21,17 @@ __device__ __forceinline__ void decode_rs(int R, long k, int& m, int& s) {
 }
 
 // H-combination of a projection A (extended layout, block m): H_s = -s eps_{s+1} A_{s+1} + (s+1) eps_s A_{s-1}
+// (the lower neighbour's load is clamped rather than branched, so all loads issue together)
 __device__ __forceinline__ double2 hcomb(const double2* __restrict__ A, const double* __restrict__ eps, long bx,
                                          int m, int s) {
     const int t = s - m;
     const double fu = -(double)s * eps[bx + t + 1];
     const double2 up = A[bx + t + 1];
+    const double el = eps[bx + t];
+    const double2 lo = A[bx + (t > 0 ? t - 1 : 0)];
     double2 h = make_double2(fu * up.x, fu * up.y);
     if (t > 0) {
-        const double fl = (s + 1.0) * eps[bx + t];
-        const double2 lo = A[bx + t - 1];
+        const double fl = (s + 1.0) * el;
         h.x += fl * lo.x;
         h.y += fl * lo.y;
     }
