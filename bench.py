@@ -12,10 +12,11 @@ Headline metric (BASELINE.json): SWE RHS evals/s (fp64 SH fwd+inv) at T255.
 Side results on the same JSON line:
   e2e            same metric through the public C ABI (pswe_eval_imex) with pinned HOST buffers,
                  every step's H2D + D2H inside the timed region (double-buffered on copy streams);
-  roofline       dominant (longest) stage's algorithmic work / its event-timed duration: FP64
-                 flops vs the FP64 DMMA peak measured in-run for the Legendre stages (MEASURED_
-                 PEAKS.json has no FP64 figure), bytes vs MEASURED_PEAKS.json hbm_gbs for the
-                 grid stage and the tail; every stage is listed under roofline.stages;
+  roofline       dominant (longest) kernel's algorithmic work / its event-timed duration: FP64
+                 flops vs the FP64 DMMA peak measured in-run for the two Legendre contractions
+                 (MEASURED_PEAKS.json has no FP64 figure), bytes vs MEASURED_PEAKS.json hbm_gbs
+                 for the coefficient prep, the grid stage and the tail; all five kernels are
+                 listed under roofline.kernels;
   cpu_baseline   the reference (oracle/_ref, compiled from /root/reference) timed on the host
                  cores, rank 0 at N=1 only;
   pfasst         config-3 PFASST block (T255 256x512 / T127 128x256, 5/3 nodes, dt 60 s, 8 steps, 4 its),
@@ -274,20 +275,22 @@ def run_ours(args):
     del dplan
 
     # per-kernel durations (same workload, L2 flushed) for the roofline
-    stage = np.zeros(4)
-    ms4 = (ctypes.c_float * 4)()
+    stage = np.zeros(5)
+    ms5 = (ctypes.c_float * 5)()
     for k in range(args.steps):
         flush.zero_()
-        _lib.check(L.pswe_eval_imex_timed(plan.handle, ctypes.byref(cprm), states.data_ptr(), fi.data_ptr(),
-                                          fe.data_ptr(), BATCH, _stream(), ms4))
-        stage += np.array(list(ms4))
+        _lib.check(L.pswe_eval_imex_kernel_times(plan.handle, ctypes.byref(cprm), states.data_ptr(), fi.data_ptr(),
+                                                 fe.data_ptr(), BATCH, _stream(), ms5))
+        stage += np.array(list(ms5))
     stage /= args.steps
     F_L = NLAT * (R_BENCH + 1) * (R_BENCH + 2)  # flops per complex field per direction
     rowb = (R_BENCH + 1) * NLAT * 16               # bytes of one field's Fourier rows (m <= R)
     Kb = P.num_coeffs(R_BENCH) * 16                # bytes of one spectral field
-    # per-stage algorithmic work: the Legendre stages are FP64-tensor
-    # bound (flops), the grid stage and the tail stream bytes (HBM)
+    Kxb = (R_BENCH + 1) * (R_BENCH + 4) // 2 * 16  # bytes of one extended-triangle column
+    # per-kernel algorithmic work: the Legendre contractions are FP64-
+    # tensor bound (flops), the prep, the grid stage and the tail stream bytes (HBM)
     work = {
+        "prep": ("hbm", BATCH * (3 * Kb + 4 * Kxb)),               # state in, 4 inverse columns out
         "legendre_inverse": ("tensor", 4 * BATCH * F_L),           # Phi, zeta, U, V
         "fft_products": ("hbm", (4 + 5) * BATCH * rowb),            # 4 fields in, 5 products out
         "legendre_forward": ("tensor", 5 * BATCH * F_L),           # Phi'U, Phi'V, qU, qV, ke
@@ -304,7 +307,7 @@ def run_ours(args):
         hbm_peak, hbm_src = float(mp["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (burst copy)"
     except Exception:
         pass
-    try:  # per-launch DRAM traffic of each stage's kernels from the committed ncu --set full capture
+    try:  # per-launch DRAM traffic of each kernel from the committed ncu --set full capture
         traffic_tab = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["stages"]
     except Exception:
         traffic_tab = {}
@@ -329,7 +332,7 @@ def run_ours(args):
                         else hbm_src),
         "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum per launch, "
                           "ncu --set full, cache flushed)",
-        "stages": stages,
+        "kernels": stages,
     }
 
     # e2e through the public C ABI (pswe_eval_imex, the drop-in boundary) with pinned host

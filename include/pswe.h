@@ -105,6 +105,11 @@ int pswe_solve_implicit(int truncation, const pswe_params* p, const double* b, d
  * tail). Measurement aid for the roofline. */
 int pswe_eval_imex_timed(pswe_plan* plan, const pswe_params* p, const double* state, double* f_imp,
                          double* f_exp, int n_states, void* stream, float* ms_out);
+/* the same with the inverse stage split into its two kernels: ms_out[5] = coefficient prep,
+ * inverse Legendre contraction, FFT+products, forward Legendre, tail (prep = 0 when the
+ * recurrence inverse runs, nlat > 512) */
+int pswe_eval_imex_kernel_times(pswe_plan* plan, const pswe_params* p, const double* state, double* f_imp,
+                                double* f_exp, int n_states, void* stream, float* ms_out);
 
 /* ---- SDC level: LevelSpec + SpaceTimeState on the device (sdc.hpp:14-45) */
 int pswe_level_create(pswe_plan* plan, const pswe_params* p, int num_nodes, pswe_level** out);

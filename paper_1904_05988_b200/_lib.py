@@ -85,6 +85,8 @@ SIGNATURES = {
     "pswe_fp64_peak": (_d, [_i, _i]),
     "pswe_eval_imex_timed": (_i, [_vp, ctypes.POINTER(Params), _vp, _vp, _vp, _i, _vp,
                                   ctypes.POINTER(ctypes.c_float)]),
+    "pswe_eval_imex_kernel_times": (_i, [_vp, ctypes.POINTER(Params), _vp, _vp, _vp, _i, _vp,
+                                  ctypes.POINTER(ctypes.c_float)]),
 }
 
 _lib = None

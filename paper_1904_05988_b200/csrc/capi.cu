@@ -193,6 +193,42 @@ int pswe_eval_imex_timed(pswe_plan* P, const pswe_params* p, const double* state
     });
 }
 
+// Per-kernel device times (ms) of one eval_imex: ms_out[5] = prep, inverse contraction, grid stage,
+// forward contraction, tail (prep = 0 and the inverse time covers both when the recurrence
+// inverse runs, J > 256). CUDA events between the launches on `stream`; synchronises.
+int pswe_eval_imex_kernel_times(pswe_plan* P, const pswe_params* p, const double* state, double* f_imp,
+                                double* f_exp, int n, void* stream, float* ms_out) {
+    return guarded([&] {
+        need(P, "plan");
+        need(p, "params");
+        need(ms_out, "ms_out");
+        const cudaStream_t st = as_stream(stream);
+        P->reserve(n);
+        cudaEvent_t ev[6];
+        for (auto& e : ev) PSWE_CUDA(cudaEventCreate(&e));
+        PSWE_CUDA(cudaEventRecord(ev[0], st));
+        if (P->legendre_mode == PSWE_LEGENDRE_STREAM && !P->simt && P->J <= 256) {
+            legendre_inverse_stream(*P, INV_EVAL, c2(state), nullptr, 4 * n, p->radius, P->d_four_a, st, ev[1]);
+        } else {
+            PSWE_CUDA(cudaEventRecord(ev[1], st));
+            legendre_inverse(*P, INV_EVAL, c2(state), nullptr, n, p->radius, P->d_four_a, st);
+        }
+        PSWE_CUDA(cudaEventRecord(ev[2], st));
+        const bool gt = gt_path_ok(*P, n);
+        if (gt) fft_eval_products_gt(*P, *p, P->d_four_a, n, st);
+        else fft_eval_products(*P, *p, P->d_four_a, P->d_four_b, n, st);
+        PSWE_CUDA(cudaEventRecord(ev[3], st));
+        if (gt) legendre_forward_gt(*P, n, P->d_proj, st);
+        else legendre_forward(*P, P->d_four_b, 5, n, P->d_proj, true, st);
+        PSWE_CUDA(cudaEventRecord(ev[4], st));
+        eval_tail(*P, *p, P->d_proj, c2(state), c2(f_imp), c2(f_exp), n, st);
+        PSWE_CUDA(cudaEventRecord(ev[5], st));
+        PSWE_CUDA(cudaEventSynchronize(ev[5]));
+        for (int i = 0; i < 5; ++i) PSWE_CUDA(cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]));
+        for (auto& e : ev) cudaEventDestroy(e);
+    });
+}
+
 int pswe_solve_implicit(int R, const pswe_params* p, const double* b, double c, double* out, int n, void* stream) {
     return guarded([&] {
         need(p, "params");

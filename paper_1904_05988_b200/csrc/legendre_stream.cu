@@ -837,7 +837,7 @@ void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, do
 
 // kind/nq/in/in2/radius as legendre_inverse_mma: tiled prep, then the TMA-pipelined contraction.
 void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq,
-                             double radius, double2* out, cudaStream_t st) {
+                             double radius, double2* out, cudaStream_t st, cudaEvent_t after_prep) {
     if (nq <= 0) return;
     const int NT = inv_choose_nt(P, nq);
     const int NQ = 4 * NT, SX = 8 * NT + 2;
@@ -867,6 +867,7 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
         launch_pdl(xtile_prep_kernel<INV_PLAIN>, g, dim3(CH * ipb), 0, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m,
                    P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     PSWE_LAUNCH_CHECK();
+    if (after_prep) PSWE_CUDA(cudaEventRecord(after_prep, st));
 #ifdef PSWE_DIAG_NOINV
     return;
 #endif

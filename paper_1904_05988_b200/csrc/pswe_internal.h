@@ -200,8 +200,9 @@ void build_legendre_checkpoints(pswe_plan& P);
 void build_legendre_table2(pswe_plan& P);
 void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
                              cudaStream_t st);
+// after_prep (optional): recorded between the prep and the contraction kernel (timing)
 void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq,
-                             double radius, double2* out, cudaStream_t st);
+                             double radius, double2* out, cudaStream_t st, cudaEvent_t after_prep = nullptr);
 
 // fft.cu
 // Fourier rows [b][m][i] -> grid [b][i][j] (c2r, Im G_0 := 0), optional per-row 1/cos(phi).

@@ -7,7 +7,7 @@ import json
 import subprocess
 import sys
 
-STAGES = {"xtile_prep": "legendre_inverse", "leg_inv": "legendre_inverse", "fft_eval": "fft_products",
+STAGES = {"xtile_prep": "prep", "leg_inv": "legendre_inverse", "fft_eval": "fft_products",
           "leg_fwd": "legendre_forward", "eval_tail": "tail"}
 
 
