@@ -107,7 +107,7 @@ int pswe_eval_imex_timed(pswe_plan* plan, const pswe_params* p, const double* st
                          double* f_exp, int n_states, void* stream, float* ms_out);
 /* the same with the inverse stage split into its two kernels: ms_out[5] = coefficient prep,
  * inverse Legendre contraction, FFT+products, forward Legendre, tail (prep = 0 when the
- * recurrence inverse runs, nlat > 512) */
+ * recurrence inverse runs: single states on grids above 768 latitudes) */
 int pswe_eval_imex_kernel_times(pswe_plan* plan, const pswe_params* p, const double* state, double* f_imp,
                                 double* f_exp, int n_states, void* stream, float* ms_out);
 

@@ -195,7 +195,7 @@ int pswe_eval_imex_timed(pswe_plan* P, const pswe_params* p, const double* state
 
 // Per-kernel device times (ms) of one eval_imex: ms_out[5] = prep, inverse contraction, grid stage,
 // forward contraction, tail (prep = 0 and the inverse time covers both when the recurrence
-// inverse runs, J > 256). CUDA events between the launches on `stream`; synchronises.
+// inverse runs: single states on grids above 768 latitudes). CUDA events between the launches on `stream`; synchronises.
 int pswe_eval_imex_kernel_times(pswe_plan* P, const pswe_params* p, const double* state, double* f_imp,
                                 double* f_exp, int n, void* stream, float* ms_out) {
     return guarded([&] {
@@ -207,7 +207,7 @@ int pswe_eval_imex_kernel_times(pswe_plan* P, const pswe_params* p, const double
         cudaEvent_t ev[6];
         for (auto& e : ev) PSWE_CUDA(cudaEventCreate(&e));
         PSWE_CUDA(cudaEventRecord(ev[0], st));
-        if (P->legendre_mode == PSWE_LEGENDRE_STREAM && !P->simt && P->J <= 256) {
+        if (!P->simt && use_stream_inverse(*P, 4 * n)) {
             legendre_inverse_stream(*P, INV_EVAL, c2(state), nullptr, 4 * n, p->radius, P->d_four_a, st, ev[1]);
         } else {
             PSWE_CUDA(cudaEventRecord(ev[1], st));

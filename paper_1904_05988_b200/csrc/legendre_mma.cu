@@ -21,6 +21,8 @@
 // fragment load two conflict-free shared-memory wavefronts.
 #include "legendre_common.cuh"
 
+#include <cstdlib>
+
 namespace pswe {
 
 namespace {
@@ -395,20 +397,27 @@ void build_legendre_checkpoints(pswe_plan& P) {
     PSWE_LAUNCH_CHECK();
 }
 
+// Streamed (TMA) inverse or the recurrence inverse. Measured (tools/stage_times.py): streamed wins
+// for every batch up to 384 latitude pairs and for batched columns (nq > 4) at every size
+// (T1023 n=5: 1029 vs 1580 us); the recurrence only for single states on the largest grids (T1023
+// n=1: 330 vs 383 us). PSWE_STREAM_INV_MAX_J overrides the size threshold (tuning only).
+bool use_stream_inverse(const pswe_plan& P, int nq) {
+    static const int maxj = [] { const char* e = std::getenv("PSWE_STREAM_INV_MAX_J"); return e ? std::atoi(e) : 384; }();
+    return P.legendre_mode == PSWE_LEGENDRE_STREAM && (P.J <= maxj || nq > 4);
+}
+
 // Inverse Legendre on DMMA. nq complex columns: PLAIN = fields, UV = 2 per pair, EVAL = 4 per state.
 void legendre_inverse_mma(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq, double radius,
                           double2* out, cudaStream_t st) {
     if (nq <= 0) return;
     if (kind == INV_PLAIN) {
-        if (P.legendre_mode == PSWE_LEGENDRE_STREAM && P.J <= 256)
+        if (use_stream_inverse(P, nq))
             legendre_inverse_stream(P, kind, in, in2, nq, radius, out, st);
         else
             dispatch_inv<false>(P, in, nq, out, st);
         return;
     }
-    // measured (tools/stage_times.py): the streamed inverse wins for J <= 256 latitude pairs, the
-    // recurrence inverse beyond (the table read is then larger than the recurrence's cost)
-    if (P.legendre_mode == PSWE_LEGENDRE_STREAM && P.J <= 256) {
+    if (use_stream_inverse(P, nq)) {
         legendre_inverse_stream(P, kind, in, in2, nq, radius, out, st);
         return;
     }

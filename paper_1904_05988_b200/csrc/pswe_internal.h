@@ -200,6 +200,8 @@ void build_legendre_checkpoints(pswe_plan& P);
 void build_legendre_table2(pswe_plan& P);
 void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext,
                              cudaStream_t st);
+// streamed (TMA) inverse chosen over the recurrence inverse for nq columns (legendre_mma.cu)
+bool use_stream_inverse(const pswe_plan& P, int nq);
 // after_prep (optional): recorded between the prep and the contraction kernel (timing)
 void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq,
                              double radius, double2* out, cudaStream_t st, cudaEvent_t after_prep = nullptr);
