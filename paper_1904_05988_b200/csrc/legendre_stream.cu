@@ -745,7 +745,15 @@ void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t s
             default: fwd_gt_launch<7, 8, 1, 2, 2>(P, gl, 5 * n, out, st); break;
         }
     } else {
-        PSWE_FWD_CASES(4, 2, 3)
+        if (gl.ntc <= 3 && P.J <= 384) {
+            // single/two-state batches up to 384 latitude pairs: 32-latitude stages (measured
+            // T511 n=1 forward 131 -> 111 us); beyond, the smaller ring keeps more blocks resident
+            // (T1023 n=1: 448 vs 498 us with 32-latitude stages)
+            if (gl.ntc == 2) fwd_gt_launch<2, 4, 2, 2, 4>(P, gl, 5 * n, out, st);
+            else fwd_gt_launch<3, 4, 2, 2, 4>(P, gl, 5 * n, out, st);
+        } else {
+            PSWE_FWD_CASES(4, 2, 3)
+        }
     }
 #undef PSWE_FWD_CASES
 }
