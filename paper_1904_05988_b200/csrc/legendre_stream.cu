@@ -299,21 +299,33 @@ __global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int n
     }
     __syncthreads();
     pdl_trigger();
-    pdl_wait();  // G tiles come from the grid stage
     const int np = npc;
-    auto issue = [&](int q) {  // stage q: latitude rows 8 SUB q .. 8 SUB q + 8 SUB - 1
+    // stage q: latitude rows 8 SUB q .. 8 SUB q + 8 SUB - 1; the P tiles (plan constants) and the G
+    // tiles (the grid stage's output) complete on the same mbarrier
+    auto issue_p = [&](int q) {
         const int k = q % S;
         constexpr unsigned PB = PS * sizeof(double);
         mbar_expect_tx(full + k, GB * (nb > 0 ? 2u : 1u) + np * PB);
-        bulk_g2s(sG + (k * 2) * gstage, ga + (long)q * gstage, GB, full + k);
-        if (nb > 0) bulk_g2s(sG + (k * 2 + 1) * gstage, gb + (long)q * gstage, GB, full + k);
         const int sub0 = q * SUB;  // first 8-latitude sub-slice: rows of slice sub0 / 4
         for (int u = 0; u < np; ++u)
             bulk_g2s(sP + (k * NS + pslot[u]) * PS, ptab + pbase[u] + (sub0 >> 2) * pstride[u] + (sub0 & 3) * 128,
                      PB, full + k);
     };
+    auto issue_g = [&](int q) {
+        const int k = q % S;
+        bulk_g2s(sG + (k * 2) * gstage, ga + (long)q * gstage, GB, full + k);
+        if (nb > 0) bulk_g2s(sG + (k * 2 + 1) * gstage, gb + (long)q * gstage, GB, full + k);
+    };
+    auto issue = [&](int q) {
+        issue_p(q);
+        issue_g(q);
+    };
+    // the first stages' P tiles stream in while the grid stage finishes (programmatic launch)
     if (threadIdx.x == 0)
-        for (int q = 0; q < S && q < nst; ++q) issue(q);
+        for (int q = 0; q < S && q < nst; ++q) issue_p(q);
+    pdl_wait();  // G tiles come from the grid stage
+    if (threadIdx.x == 0)
+        for (int q = 0; q < S && q < nst; ++q) issue_g(q);
 
     double acc[NTC][CPW][2][2];
 #pragma unroll
@@ -553,18 +565,30 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
     }
     __syncthreads();
     pdl_trigger();
-    pdl_wait();  // X tiles come from the prep kernel
     const int ngr = (nch + CPS - 1) / CPS;  // stages of CPS chunks: one copy per slice, one X copy
-    auto issue = [&](int g) {
+    auto issue_p = [&](int g) {  // P tiles: plan constants
         const int k = g % S, c0 = g * CPS, nc = min(CPS, nch - c0);
         mbar_expect_tx(full + k, nc * (nact * PB + XB));
         for (int w = 0; w < nact; ++w)
             bulk_g2s(sP + (k * WS + w) * CPS * 512, pm + ((long)w * nch + c0) * 512, nc * PB, full + k);
+    };
+    auto issue_x = [&](int g) {  // X tiles: the prep kernel's output
+        const int k = g % S, c0 = g * CPS, nc = min(CPS, nch - c0);
         bulk_g2s(sX + k * CPS * CH * SX, xm + (long)c0 * CH * SX, nc * XB, full + k);
     };
+    auto issue = [&](int g) {
+        issue_p(g);
+        issue_x(g);
+    };
+#ifndef PSWE_DIAG_NOTMA
+    // the first stages' P tiles stream in while the prep kernel finishes (programmatic launch)
+    if (threadIdx.x == 0)
+        for (int g = 0; g < S && g < ngr; ++g) issue_p(g);
+#endif
+    pdl_wait();  // X tiles come from the prep kernel
 #ifndef PSWE_DIAG_NOTMA
     if (threadIdx.x == 0)
-        for (int g = 0; g < S && g < ngr; ++g) issue(g);
+        for (int g = 0; g < S && g < ngr; ++g) issue_x(g);
 #endif
 
     double acc[2][2][NT][2];  // [m-tile 2 mh + a][parity][n-tile][v]
