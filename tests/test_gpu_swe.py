@@ -87,6 +87,22 @@ def test_large_batches_equal_single(P, R, grid, n):
         assert rel_diff_fields(fi_b[i], fi[0]) < 1e-15
 
 
+@pytest.mark.parametrize("R,grid", [(511, (768, 1536)), (1023, (1024, 2048))])
+def test_large_grid_batch_equals_single(P, R, grid):
+    """T511 / T1023: a 5-state batch (streamed TMA inverse, large-grid forward configuration) must
+    match single-state evaluations (T1023: recurrence inverse) - two independent implementations
+    of the inverse Legendre contraction checked against each other."""
+    from paper_1904_05988_b200.cases import balanced_random_state
+    plan = P.TransformPlan(R, grid[0], grid[1])
+    p = P.ModelParams(phi_bar=9.80616 * 1e4)
+    sts = np.stack([balanced_random_state(R, 30.0, 300 + s, phi_bar=p.phi_bar) for s in range(5)])
+    fi_b, fe_b = (host(t) for t in P.imex_split(cuda(sts), p, plan))
+    for i in (0, 4):
+        fi, fe = (host(t) for t in P.imex_split(cuda(sts[i:i + 1]), p, plan))
+        assert rel_diff_fields(fe_b[i], fe[0]) < 1e-12
+        assert rel_diff_fields(fi_b[i], fi[0]) < 1e-15
+
+
 def test_nonlinear_properties(P):
     """test_swe.cpp:75-129."""
     R = 15
