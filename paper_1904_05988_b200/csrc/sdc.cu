@@ -144,24 +144,30 @@ __device__ __forceinline__ void decode(int R, long k, int& m, int& s) {
     s = mm + (int)(k - off_std(R, mm));
 }
 
-// rhs (sdc.cpp:31-44, same axpy order) then solve_implicit (swe.cpp:77-98)
-__global__ void sweep_node_kernel(SweepNodeArgs A) {
+// rhs (sdc.cpp:31-44, same axpy order) then solve_implicit (swe.cpp:77-98). Block (128, 3): thread
+// (x, f) accumulates field f of coefficient k (node loops unrolled over NN nodes, loads predicated on
+// j <= m so they all issue together); field 0's thread then solves the coupled (Phi, delta) system.
+template <int NN>
+__global__ void __launch_bounds__(384) sweep_node_kernel(SweepNodeArgs A) {
+    __shared__ double2 rs[3][128];
     const long K = (long)(A.R + 1) * (A.R + 2) / 2;
-    const long k = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= K) return;
-    double2 r[3];
-#pragma unroll
-    for (int f = 0; f < 3; ++f) {
+    const long k = (long)blockIdx.x * 128 + threadIdx.x;
+    const int f = threadIdx.y;
+    if (k < K) {
         const long i = f * K + k;
         double2 acc = A.theta0[i];
-        for (int j = 1; j <= A.m; ++j) {
-            axpy(acc, A.ae[j], A.fe_new[j][i]);
-            axpy(acc, -A.ae[j], A.fe_old[j][i]);
-            axpy(acc, A.ai[j], A.fi_new[j][i]);
-            axpy(acc, -A.ai[j], A.fi_old[j][i]);
+#pragma unroll
+        for (int j = 1; j < NN; ++j) {
+            if (j <= A.m) {
+                axpy(acc, A.ae[j], A.fe_new[j][i]);
+                axpy(acc, -A.ae[j], A.fe_old[j][i]);
+                axpy(acc, A.ai[j], A.fi_new[j][i]);
+                axpy(acc, -A.ai[j], A.fi_old[j][i]);
+            }
         }
         axpy(acc, -A.aii, A.fi_old[A.m + 1][i]);
-        for (int j = 0; j <= A.M; ++j) {
+#pragma unroll
+        for (int j = 0; j < NN; ++j) {
             axpy(acc, A.aq[j], A.fi_old[j][i]);
             axpy(acc, A.aq[j], A.fe_old[j][i]);
         }
@@ -170,15 +176,18 @@ __global__ void sweep_node_kernel(SweepNodeArgs A) {
             acc.x += t.x;
             acc.y += t.y;
         }
-        r[f] = acc;
+        rs[f][threadIdx.x] = acc;
     }
+    __syncthreads();
+    if (f != 0 || k >= K) return;
+    const double2 r0 = rs[0][threadIdx.x], r1 = rs[1][threadIdx.x], r2 = rs[2][threadIdx.x];
     const int s = degree_of(A.R, k);
     const double c = A.aii;
     const double lam = -s * (s + 1.0) * A.inv_a2;
     const double diff = 1.0 - c * A.nu * lam;
-    const double2 bp = make_double2(r[0].x / diff, r[0].y / diff);
-    const double2 bz = make_double2(r[1].x / diff, r[1].y / diff);
-    const double2 bd = make_double2(r[2].x / diff, r[2].y / diff);
+    const double2 bp = make_double2(r0.x / diff, r0.y / diff);
+    const double2 bz = make_double2(r1.x / diff, r1.y / diff);
+    const double2 bd = make_double2(r2.x / diff, r2.y / diff);
     const double ce = c / diff;
     const double det = 1.0 - ce * ce * A.phi_bar * lam;
     A.out[k] = make_double2((bp.x - ce * A.phi_bar * bd.x) / det, (bp.y - ce * A.phi_bar * bd.y) / det);
@@ -195,17 +204,27 @@ struct ResidualArgs {
     long n3;  // 3K
 };
 
+// F_I, F_E of every node loaded once per coefficient and reused for all NN rows (same axpy order)
+template <int NN>
 __global__ void residual_kernel(ResidualArgs A, unsigned long long* out) {
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
     double mx = 0.0;
     if (i < A.n3) {
-        const double2 s0 = A.state[0][i];
-        for (int m = 0; m < A.nn; ++m) {
-            const double2 sm = A.state[m][i];
-            double2 acc = make_double2(sm.x - s0.x, sm.y - s0.y);
-            for (int j = 0; j < A.nn; ++j) {
-                axpy(acc, A.w[m][j], A.fi[j][i]);
-                axpy(acc, A.w[m][j], A.fe[j][i]);
+        double2 fi[NN], fe[NN], st[NN];
+#pragma unroll
+        for (int j = 0; j < NN; ++j) {
+            fi[j] = A.fi[j][i];
+            fe[j] = A.fe[j][i];
+            st[j] = A.state[j][i];
+        }
+        const double2 s0 = st[0];
+#pragma unroll
+        for (int m = 0; m < NN; ++m) {
+            double2 acc = make_double2(st[m].x - s0.x, st[m].y - s0.y);
+#pragma unroll
+            for (int j = 0; j < NN; ++j) {
+                axpy(acc, A.w[m][j], fi[j]);
+                axpy(acc, A.w[m][j], fe[j]);
             }
             mx = fmax(mx, hypot(acc.x, acc.y));
         }
@@ -238,19 +257,18 @@ struct TimeMatArgs {
     int rows, cols;
 };
 
-// y[i] = restrict( sum_j w(i,j) x[j] ) for every coarse node i (multilevel.cpp:100-107)
-__global__ void restrict_states_kernel(TimeMatArgs A, double2* const* __restrict__ dst_unused, double2* out0,
-                                       long stride_out, int Rf, int Rc) {
+// y[i] = restrict( sum_j w(i,j) x[j] ) for every coarse node i (multilevel.cpp:100-107); row i = blockIdx.y
+__global__ void restrict_states_kernel(TimeMatArgs A, double2* out0, long stride_out, int Rf, int Rc) {
     const long Kc = (long)(Rc + 1) * (Rc + 2) / 2, Kf = (long)(Rf + 1) * (Rf + 2) / 2;
     const long kc3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
     if (kc3 >= 3 * Kc) return;
     const long kf3 = fine_index(Rf, Rc, kc3, Kc, Kf);
-    for (int i = 0; i < A.rows; ++i) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int j = 0; j < A.cols; ++j)
-            if (A.w[i][j] != 0.0) axpy(acc, A.w[i][j], A.src[j][kf3]);
-        out0[i * stride_out + kc3] = acc;
-    }
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < kMaxNodes; ++j)
+        if (j < A.cols && A.w[i][j] != 0.0) axpy(acc, A.w[i][j], A.src[j][kf3]);
+    out0[i * stride_out + kc3] = acc;
 }
 
 // tau_i = dt * [ restrict(sum_j qfr(i,j)(FI_f[j] + FE_f[j])) - sum_j qc(i,j)(FI_c[j] + FE_c[j]) ]
@@ -270,34 +288,39 @@ struct FasArgs {
     int mc, mf, Rf, Rc;
     double dt;
 };
+// row i = blockIdx.y; node loops unrolled over kMaxNodes with predicated loads (same order as before)
 __global__ void fas_kernel(FasArgs A, double2* tau) {
     const long Kc = (long)(A.Rc + 1) * (A.Rc + 2) / 2, Kf = (long)(A.Rf + 1) * (A.Rf + 2) / 2;
     const long kc3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
     if (kc3 >= 3 * Kc) return;
     const long kf3 = fine_index(A.Rf, A.Rc, kc3, Kc, Kf);
-    for (int i = 0; i < A.mc; ++i) {
-        double2 acc = make_double2(0.0, 0.0);
-        for (int j = 0; j < A.mf; ++j) {
-            const double w = A.qfr[i][j];
-            if (w == 0.0) continue;
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < kMaxNodes; ++j) {
+        const double w = A.qfr[i][j];
+        if (j < A.mf && w != 0.0) {
             axpy(acc, w, A.fi_f[j][kf3]);
             axpy(acc, w, A.fe_f[j][kf3]);
         }
-        for (int j = 0; j < A.mc; ++j) {
-            const double w = A.qc[i][j];
-            if (w == 0.0) continue;
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxNodes; ++j) {
+        const double w = A.qc[i][j];
+        if (j < A.mc && w != 0.0) {
             axpy(acc, -w, A.fi_c[j][kc3]);
             axpy(acc, -w, A.fe_c[j][kc3]);
         }
-        double2 t = make_double2(acc.x * A.dt, acc.y * A.dt);
-        if (A.tau_f) {
-            for (int j = 0; j < A.mf; ++j) {
-                const double w = A.tr[i][j];
-                if (w != 0.0) axpy(t, w, A.tau_f[j * 3 * Kf + kf3]);
-            }
-        }
-        tau[i * 3 * Kc + kc3] = t;
     }
+    double2 t = make_double2(acc.x * A.dt, acc.y * A.dt);
+    if (A.tau_f) {
+#pragma unroll
+        for (int j = 0; j < kMaxNodes; ++j) {
+            const double w = A.tr[i][j];
+            if (j < A.mf && w != 0.0) axpy(t, w, A.tau_f[j * 3 * Kf + kf3]);
+        }
+    }
+    tau[i * 3 * Kc + kc3] = t;
 }
 
 // fine[i] (+)= sum_j ti(i,j) pad(a[j] - b[j])  (interpolate_increment / interpolate_states,
@@ -311,40 +334,40 @@ struct InterpArgs {
     int mf, mc, Rf, Rc, nfam;
     double2* dstate0;  // optional: node-0 state increment (fine layout)
 };
+// one (family, fine node) pair per blockIdx.y: blockIdx.y = fam * mf + i
 __global__ void interp_kernel(InterpArgs A, int mode) {
     const long Kc = (long)(A.Rc + 1) * (A.Rc + 2) / 2, Kf = (long)(A.Rf + 1) * (A.Rf + 2) / 2;
     const long kf3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int fam = blockIdx.y / A.mf, i = blockIdx.y - fam * A.mf;
     if (kf3 >= 3 * Kf) return;
     const int f = (int)(kf3 / Kf);
     const long kf = kf3 - f * Kf;
     int m, s;
     decode(A.Rf, kf, m, s);
     const bool inside = (m <= A.Rc && s <= A.Rc);
-    const long kc3 = inside ? f * Kc + off_std(A.Rc, m) + (s - m) : 0;
-    for (int fam = 0; fam < A.nfam; ++fam) {
-        for (int i = 0; i < A.mf; ++i) {
-            double2 acc = make_double2(0.0, 0.0);
-            if (inside) {
-                for (int j = 0; j < A.mc; ++j) {
-                    const double w = A.w[i][j];
-                    if (w == 0.0) continue;
-                    double2 d = A.a[fam][j][kc3];
-                    if (mode == 0) {
-                        const double2 sv = A.b[fam][j][kc3];
-                        d = make_double2(d.x - sv.x, d.y - sv.y);
-                    }
-                    axpy(acc, w, d);
+    double2 acc = make_double2(0.0, 0.0);
+    if (inside) {
+        const long kc3 = f * Kc + off_std(A.Rc, m) + (s - m);
+#pragma unroll
+        for (int j = 0; j < kMaxNodes; ++j) {
+            const double w = A.w[i][j];
+            if (j < A.mc && w != 0.0) {
+                double2 d = A.a[fam][j][kc3];
+                if (mode == 0) {
+                    const double2 sv = A.b[fam][j][kc3];
+                    d = make_double2(d.x - sv.x, d.y - sv.y);
                 }
-            }
-            double2* o = A.dst[fam][i] + kf3;
-            if (mode == 0) {
-                const double2 cur = *o;
-                *o = make_double2(cur.x + acc.x, cur.y + acc.y);
-                if (fam == 0 && i == 0 && A.dstate0) A.dstate0[kf3] = acc;
-            } else {
-                *o = acc;
+                axpy(acc, w, d);
             }
         }
+    }
+    double2* o = A.dst[fam][i] + kf3;
+    if (mode == 0) {
+        const double2 cur = *o;
+        *o = make_double2(cur.x + acc.x, cur.y + acc.y);
+        if (fam == 0 && i == 0 && A.dstate0) A.dstate0[kf3] = acc;
+    } else {
+        *o = acc;
     }
 }
 
@@ -404,8 +427,13 @@ void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) 
         A.inv_a2 = 1.0 / (L->prm.radius * L->prm.radius);
         A.phi_bar = L->prm.phi_bar;
         A.nu = L->prm.nu;
-        const int bs = 128;
-        sweep_node_kernel<<<(unsigned)((L->K + bs - 1) / bs), bs, 0, st>>>(A);
+        const dim3 grid((unsigned)((L->K + 127) / 128)), block(128, 3);
+        switch (L->nn) {
+            case 2: sweep_node_kernel<2><<<grid, block, 0, st>>>(A); break;
+            case 3: sweep_node_kernel<3><<<grid, block, 0, st>>>(A); break;
+            case 4: sweep_node_kernel<4><<<grid, block, 0, st>>>(A); break;
+            default: sweep_node_kernel<5><<<grid, block, 0, st>>>(A); break;
+        }
         PSWE_LAUNCH_CHECK();
         eval_imex(*L->plan, L->prm, L->st(m + 1), L->fi(m + 1, nw), L->fe(m + 1, nw), 1, st);
     }
@@ -424,7 +452,14 @@ void level_residual(pswe_level* L, double dt, double* out, cudaStream_t st) {
     }
     PSWE_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
     const int bs = 256;
-    residual_kernel<<<(unsigned)((A.n3 + bs - 1) / bs), bs, 0, st>>>(A, reinterpret_cast<unsigned long long*>(out));
+    const unsigned g = (unsigned)((A.n3 + bs - 1) / bs);
+    auto* o = reinterpret_cast<unsigned long long*>(out);
+    switch (L->nn) {
+        case 2: residual_kernel<2><<<g, bs, 0, st>>>(A, o); break;
+        case 3: residual_kernel<3><<<g, bs, 0, st>>>(A, o); break;
+        case 4: residual_kernel<4><<<g, bs, 0, st>>>(A, o); break;
+        default: residual_kernel<5><<<g, bs, 0, st>>>(A, o); break;
+    }
     PSWE_LAUNCH_CHECK();
 }
 
@@ -437,7 +472,8 @@ void pair_restrict_states(pswe_pair* P, cudaStream_t st) {
     for (int i = 0; i < C->nn; ++i)
         for (int j = 0; j < F->nn; ++j) A.w[i][j] = P->tr[(size_t)i * F->nn + j];
     const long n = 3 * C->K;
-    restrict_states_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(A, nullptr, C->st(0), 3 * C->K, F->R, C->R);
+    restrict_states_kernel<<<dim3((unsigned)((n + 127) / 128), C->nn), 128, 0, st>>>(A, C->st(0), 3 * C->K, F->R,
+                                                                                   C->R);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -464,7 +500,7 @@ void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st, const doub
         for (int j = 0; j < C->nn; ++j) A.qc[i][j] = C->tab.Q(i, j);
     }
     const long n = 3 * C->K;
-    fas_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(A, tau);
+    fas_kernel<<<dim3((unsigned)((n + 127) / 128), C->nn), 128, 0, st>>>(A, tau);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -498,7 +534,7 @@ void pair_interp_increment_add(pswe_pair* P, double2* dstate0, cudaStream_t st) 
         for (int j = 0; j < C->nn; ++j) A.w[i][j] = P->ti[(size_t)i * C->nn + j];
     }
     const long n = 3 * F->K;
-    interp_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(A, 0);
+    interp_kernel<<<dim3((unsigned)((n + 127) / 128), 3 * F->nn), 128, 0, st>>>(A, 0);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -516,7 +552,7 @@ void pair_interp_states(pswe_pair* P, cudaStream_t st) {
         for (int j = 0; j < C->nn; ++j) A.w[i][j] = P->ti[(size_t)i * C->nn + j];
     }
     const long n = 3 * F->K;
-    interp_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(A, 1);
+    interp_kernel<<<dim3((unsigned)((n + 127) / 128), F->nn), 128, 0, st>>>(A, 1);
     PSWE_LAUNCH_CHECK();
 }
 
