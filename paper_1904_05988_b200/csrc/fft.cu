@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(256) fft_eval_kernel(FftDesc fd, int R, int nl
 void fft_rows_c2r(const pswe_plan& P, const double2* four, int in_stride, int in_off, double* grid, int n,
                   bool div_cos, cudaStream_t st) {
     if (n <= 0) return;
+    if (fft_rows_ip(P, true, four, nullptr, nullptr, grid, in_stride, in_off, n, div_cos, 0, 1.0, st)) return;
     if (fft_rows_c2r_t(P, four, in_stride, in_off, grid, n, div_cos, st)) return;
     const size_t sm = 2 * (size_t)P.N * sizeof(double2);
     if (sm > 48 * 1024) PSWE_CUDA(cudaFuncSetAttribute(fft_c2r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -264,6 +265,8 @@ void fft_rows_c2r(const pswe_plan& P, const double2* four, int in_stride, int in
 void fft_rows_r2c(const pswe_plan& P, const double* grid, double2* four, int out_stride, int out_off, int n,
                   bool pre_cos, int scale_mode, double radius, cudaStream_t st) {
     if (n <= 0) return;
+    if (fft_rows_ip(P, false, nullptr, grid, four, nullptr, out_stride, out_off, n, pre_cos, scale_mode, radius, st))
+        return;
     if (fft_rows_r2c_t(P, grid, four, out_stride, out_off, n, pre_cos, scale_mode, radius, st)) return;
     const size_t sm = 2 * (size_t)P.N * sizeof(double2);
     if (sm > 48 * 1024) PSWE_CUDA(cudaFuncSetAttribute(fft_r2c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

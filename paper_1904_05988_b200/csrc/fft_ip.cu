@@ -317,7 +317,187 @@ bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, dou
     return true;
 }
 
+// slot of frequency k after the DIF passes (k = d0 + P0 d1 + P0 P1 d2 -> d0 M0 + d1 M1 + d2 M2):
+// the mixed-radix digit reversal of the in-place plan
+template <int N>
+__device__ __forceinline__ int ip_slot(int k) {
+    int p = 0;
+#pragma unroll
+    for (int s = 0; s < ip_npass(N); ++s) {
+        const int P = ip_radix(N, s), M = ip_len(N, s) / P;
+        p += (k % P) * M;
+        k /= P;
+    }
+    return p;
+}
+
+// rows of one field per block: 8 consecutive latitudes up to N = 512 (so the [q][m][i] Fourier
+// writes of r2c are 128-byte runs), fewer beyond (shared memory)
+__host__ __device__ constexpr int ip_rows(int N) { return N <= 512 ? 8 : (N <= 1024 ? 4 : 2); }
+
+// Plain longitude transforms of ROWS consecutive latitude rows of one field (synthesise / analyse /
+// uv_from_vortdiv / vortdiv_from_uv, transform.cpp:101-190), in place in shared memory.
+// C2R: Fourier rows [q][i][m] (q = b in_stride + in_off) -> c2r pre-pass written straight to the
+//      digit-reversed slots -> inverse DIT passes -> natural-order grid rows (optionally / cos).
+// R2C: grid rows (optionally * cos) -> forward DIF passes -> r2c post-pass gathered from the
+//      digit-reversed slots, scaled (scale_mode 0: w / nlon, 1: w / (a cos^2 nlon)), staged
+//      [m][row] in shared memory -> Fourier rows [q][m][i] (q = b out_stride + out_off).
+template <int N, bool C2R>
+__global__ void __launch_bounds__(kIpThreads)
+    fft_rows_ip_kernel(int R, int nlat, const double2* __restrict__ TW, const double2* __restrict__ post,
+                       const double2* __restrict__ four_in, const double* __restrict__ grid_in, double2* __restrict__ four_out,
+                       double* __restrict__ grid_out, int stride, int off, const double* __restrict__ rowc,
+                       const double* __restrict__ roww, int cos_flag, int scale_mode, double inv_a) {
+    constexpr int ROWS = ip_rows(N), RS = ipadded(N);
+    extern __shared__ double2 A[];  // [ROWS][N] ipad layout (R2C: then the [R+1][ROWS] staging); twiddles
+    double2* sTW = A + ROWS * RS;
+    const int i0 = blockIdx.x * ROWS, b = blockIdx.y;
+    const int nrow = min(ROWS, nlat - i0);
+    for (int t = threadIdx.x; t < ip_ntw(N); t += kIpThreads) {
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sTW + t));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(TW + t));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    if constexpr (C2R) {
+        const double2* in = four_in + (((long)b * stride + off) * nlat + i0) * (R + 1);  // row r: + r (R + 1)
+        constexpr int H = N / 2 + 1;
+        constexpr int HS = (H + 7) & ~7;
+        constexpr int U = (ROWS * HS + kIpThreads - 1) / kIpThreads;
+        double2 xa[U], xb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int it = threadIdx.x + u * kIpThreads;
+            const int r = it / HS, k = it - r * HS;
+            xa[u] = xb[u] = make_double2(0.0, 0.0);
+            if (r < nrow && k < H) {
+                if (k <= R) xa[u] = in[(long)r * (R + 1) + k];
+                if (k > 0 && N - k <= R) xb[u] = in[(long)r * (R + 1) + N - k];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int it = threadIdx.x + u * kIpThreads;
+            const int r = it / HS, k = it - r * HS;
+            if (r < ROWS && k < H) {
+                double2 a = xa[u];
+                if (k == 0) a.y = 0.0;
+                A[ipad(r * N + ip_slot<N>(k))] = c2r_z(a, xb[u], __ldg(post + k));
+                if (k > 0 && k < N / 2) A[ipad(r * N + ip_slot<N>(N - k))] = c2r_z(xb[u], xa[u], __ldg(post + N - k));
+            }
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();
+        DitGuard<N, ip_npass(N) - 1, ROWS, true>::run(A, sTW);
+        for (int it = threadIdx.x; it < ROWS * N; it += kIpThreads) {
+            const int r = it / N, k = it - r * N;
+            if (r >= nrow) break;
+            double2 v = A[ipad(it)];
+            if (cos_flag) {
+                const double cc = 1.0 / rowc[i0 + r];
+                v = make_double2(v.x * cc, v.y * cc);
+            }
+            reinterpret_cast<double2*>(grid_out + ((long)b * nlat + i0 + r) * 2 * N)[k] = v;
+        }
+    } else {
+        const double2* in = reinterpret_cast<const double2*>(grid_in + ((long)b * nlat + i0) * 2 * N);
+        constexpr int UL = (ROWS * N + kIpThreads - 1) / kIpThreads;
+        double2 v[UL];
+#pragma unroll
+        for (int u = 0; u < UL; ++u) {
+            const int it = threadIdx.x + u * kIpThreads;
+            v[u] = (it < ROWS * N && it / N < nrow) ? in[it] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < UL; ++u) {
+            const int it = threadIdx.x + u * kIpThreads;
+            if (it >= ROWS * N) break;
+            if (cos_flag && it / N < nrow) {
+                const double c = rowc[i0 + it / N];
+                v[u] = make_double2(v[u].x * c, v[u].y * c);
+            }
+            A[ipad(it)] = v[u];
+        }
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();
+        DifGuard<N, 0, ROWS, false>::run(A, sTW);
+        // post-pass into registers, then staged [m][row] over the rows (row index XOR-swizzled
+        // with m: conflict-free for both the m-fastest writes and the row-fastest reads)
+        constexpr int UP = (ROWS * N + kIpThreads - 1) / kIpThreads;  // >= ROWS (R + 1) / 256
+        double2 xr[UP];
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+            const int it = threadIdx.x + u * kIpThreads;
+            const int r = it / (R + 1), k = it - r * (R + 1);
+            if (r < ROWS) {
+                const double2 zk = A[ipad(r * N + ip_slot<N>(k))];
+                const double2 zc = cconj(A[ipad(r * N + ip_slot<N>(k == 0 ? 0 : N - k))]);
+                const double2 e = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
+                const double2 d = csub(zk, zc);
+                const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);
+                xr[u] = cadd(e, cmul(__ldg(post + k), o));
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+            const int it = threadIdx.x + u * kIpThreads;
+            const int r = it / (R + 1), k = it - r * (R + 1);
+            if (r < ROWS) A[k * ROWS + (r ^ (k & (ROWS - 1)))] = xr[u];
+        }
+        __syncthreads();
+        const double nl = 2.0 * N;
+        double2* out = four_out + ((long)b * stride + off) * (R + 1) * nlat + i0;
+        for (int it = threadIdx.x; it < ROWS * (R + 1); it += kIpThreads) {
+            const int k = it / ROWS, r = it - k * ROWS;
+            if (r >= nrow) continue;
+            const int i = i0 + r;
+            const double c = rowc[i];
+            const double sc = scale_mode == 0 ? (1.0 / nl) * roww[i] : (1.0 / nl) * (inv_a * roww[i] / (c * c));
+            const double2 x = A[k * ROWS + (r ^ (k & (ROWS - 1)))];
+            out[(long)k * nlat + r] = make_double2(x.x * sc, x.y * sc);
+        }
+    }
+}
+
+template <int N, bool C2R>
+bool rows_ip(const pswe_plan& P, const double2* four_in, const double* grid_in, double2* four_out, double* grid_out,
+             int stride, int off, int n, int cos_flag, int scale_mode, double inv_a, cudaStream_t st) {
+    constexpr int ROWS = ip_rows(N);
+    const size_t sm = (size_t)(ROWS * ipadded(N) + ip_ntw(N)) * sizeof(double2);
+    if (sm > 227 * 1024) return false;
+    auto kern = fft_rows_ip_kernel<N, C2R>;
+    static bool attr = false;  // once per instantiation (the cap, not the size of this launch)
+    if (!attr) {
+        PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    kern<<<dim3((P.nlat + ROWS - 1) / ROWS, n), kIpThreads, sm, st>>>(
+        P.R, P.nlat, P.d_fft_iptw, P.d_fft_post, four_in, grid_in, four_out, grid_out, stride, off, P.d_rowc,
+        P.d_roww, cos_flag, scale_mode, inv_a);
+    PSWE_LAUNCH_CHECK();
+    return true;
+}
+
 }  // namespace
+
+bool fft_rows_ip(const pswe_plan& P, bool c2r, const double2* four_in, const double* grid_in, double2* four_out,
+                 double* grid_out, int stride, int off, int n, bool cos_flag, int scale_mode, double radius,
+                 cudaStream_t st) {
+    static const bool off_env = [] { const char* e = getenv("PSWE_FFT_STOCKHAM"); return e && atoi(e) != 0; }();
+    if (off_env) return false;
+    const int cf = cos_flag ? 1 : 0;
+    const double ia = 1.0 / radius;
+    switch (P.N) {
+#define PSWE_CASE(NN)                                                                                        \
+    case NN:                                                                                                 \
+        return c2r ? rows_ip<NN, true>(P, four_in, grid_in, four_out, grid_out, stride, off, n, cf, scale_mode, ia, st) \
+                   : rows_ip<NN, false>(P, four_in, grid_in, four_out, grid_out, stride, off, n, cf, scale_mode, ia, st);
+        PSWE_CASE(24) PSWE_CASE(32) PSWE_CASE(48) PSWE_CASE(64) PSWE_CASE(96) PSWE_CASE(128) PSWE_CASE(192)
+        PSWE_CASE(256) PSWE_CASE(384) PSWE_CASE(512) PSWE_CASE(768) PSWE_CASE(1024) PSWE_CASE(1536)
+#undef PSWE_CASE
+        default: return false;
+    }
+}
 
 // Twiddles of the in-place plan: pass s (P, M, n = P M): entries OFF_s + (k-1) M + j =
 // exp(-2 pi i j k / n), k = 1..P-1, j = 0..M-1. Empty (one dummy entry) if N has no plan.

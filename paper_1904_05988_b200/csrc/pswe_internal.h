@@ -234,6 +234,10 @@ bool fft_eval_products_ip(const pswe_plan& P, const pswe_params& prm, const doub
                           cudaStream_t st);
 bool fft_eval_products_t(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
                          cudaStream_t st);
+// in-place plain row transforms (fft_ip.cu); false when nlon/2 has no in-place plan
+bool fft_rows_ip(const pswe_plan& P, bool c2r, const double2* four_in, const double* grid_in, double2* four_out,
+                 double* grid_out, int stride, int off, int n, bool cos_flag, int scale_mode, double radius,
+                 cudaStream_t st);
 bool fft_rows_c2r_t(const pswe_plan& P, const double2* four, int in_stride, int in_off, double* grid, int n,
                     bool div_cos, cudaStream_t st);
 bool fft_rows_r2c_t(const pswe_plan& P, const double* grid, double2* four, int out_stride, int out_off, int n,

@@ -25,7 +25,7 @@ def main():
     rx = sys.argv[2] if len(sys.argv) > 2 else '.'
     rows = list(csv.reader(io.StringIO(ncu('-i', rep, '--page', 'raw', '--csv'))))
     hdr, units = rows[0], rows[1]
-    for r in rows[2:]:
+    for idx, r in enumerate(rows[2:]):
         name = r[hdr.index('Kernel Name')]
         if not re.search(rx, name):
             continue
@@ -44,8 +44,9 @@ def main():
         tot = sum(v for v, _ in st) or 1
         print('  stalls:', ', '.join(f"{h} {v / tot * 100:.0f}%" for v, h in st[:7]))
         kname = re.sub(r'\(.*', '', name).split('::')[-1].split('<')[0]
-        src = list(csv.reader(io.StringIO(ncu('-i', rep, '--page', 'source', '--csv', '--kernel-name',
-                                              f'regex:{kname}', '--print-source', 'cuda,sass'))))
+        # this launch only (a name regex would merge template instantiations)
+        src = list(csv.reader(io.StringIO(ncu('-i', rep, '--page', 'source', '--csv', '--launch-skip', str(idx),
+                                              '--launch-count', '1', '--print-source', 'cuda,sass'))))
         out, fname = [], ''
         for s in src:
             if len(s) >= 2 and s[0] == 'File Path':
