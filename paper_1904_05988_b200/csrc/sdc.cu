@@ -111,6 +111,8 @@ struct SweepNodeArgs {
     double ae[kMaxNodes], ai[kMaxNodes];  // dt*qE(m+1,j), dt*qI(m+1,j), j = 1..m
     double aq[kMaxNodes];                 // dt*q(m+1,j), j = 0..M
     double aii;                           // dt*qI(m+1,m+1)
+    double2* fi0_dst;                     // node 0's F_I, F_E copied old -> new buffer (first node only)
+    double2* fe0_dst;
     int m, M, R;
     double inv_a2, phi_bar, nu;
 };
@@ -153,6 +155,8 @@ __global__ void __launch_bounds__(384) sweep_node_kernel(SweepNodeArgs A) {
     const long K = (long)(A.R + 1) * (A.R + 2) / 2;
     const long k = (long)blockIdx.x * 128 + threadIdx.x;
     const int f = threadIdx.y;
+    pdl_trigger();
+    pdl_wait();  // F and states come from the preceding evaluation
     if (k < K) {
         const long i = f * K + k;
         double2 acc = A.theta0[i];
@@ -168,8 +172,13 @@ __global__ void __launch_bounds__(384) sweep_node_kernel(SweepNodeArgs A) {
         axpy(acc, -A.aii, A.fi_old[A.m + 1][i]);
 #pragma unroll
         for (int j = 0; j < NN; ++j) {
-            axpy(acc, A.aq[j], A.fi_old[j][i]);
-            axpy(acc, A.aq[j], A.fe_old[j][i]);
+            const double2 fij = A.fi_old[j][i], fej = A.fe_old[j][i];
+            axpy(acc, A.aq[j], fij);
+            axpy(acc, A.aq[j], fej);
+            if (j == 0 && A.fi0_dst) {  // node 0 keeps its right-hand sides (sdc.cpp:22-29)
+                A.fi0_dst[i] = fij;
+                A.fe0_dst[i] = fej;
+            }
         }
         if (A.tau) {
             const double2 t = A.tau[i];
@@ -208,6 +217,8 @@ struct ResidualArgs {
 template <int NN>
 __global__ void residual_kernel(ResidualArgs A, unsigned long long* out) {
     const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_trigger();
+    pdl_wait();
     double mx = 0.0;
     if (i < A.n3) {
         double2 fi[NN], fe[NN], st[NN];
@@ -262,6 +273,8 @@ __global__ void restrict_states_kernel(TimeMatArgs A, double2* out0, long stride
     const long Kc = (long)(Rc + 1) * (Rc + 2) / 2, Kf = (long)(Rf + 1) * (Rf + 2) / 2;
     const long kc3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const int i = blockIdx.y;
+    pdl_trigger();
+    pdl_wait();
     if (kc3 >= 3 * Kc) return;
     const long kf3 = fine_index(Rf, Rc, kc3, Kc, Kf);
     double2 acc = make_double2(0.0, 0.0);
@@ -293,6 +306,8 @@ __global__ void fas_kernel(FasArgs A, double2* tau) {
     const long Kc = (long)(A.Rc + 1) * (A.Rc + 2) / 2, Kf = (long)(A.Rf + 1) * (A.Rf + 2) / 2;
     const long kc3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const int i = blockIdx.y;
+    pdl_trigger();
+    pdl_wait();
     if (kc3 >= 3 * Kc) return;
     const long kf3 = fine_index(A.Rf, A.Rc, kc3, Kc, Kf);
     double2 acc = make_double2(0.0, 0.0);
@@ -339,6 +354,8 @@ __global__ void interp_kernel(InterpArgs A, int mode) {
     const long Kc = (long)(A.Rc + 1) * (A.Rc + 2) / 2, Kf = (long)(A.Rf + 1) * (A.Rf + 2) / 2;
     const long kf3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const int fam = blockIdx.y / A.mf, i = blockIdx.y - fam * A.mf;
+    pdl_trigger();
+    pdl_wait();
     if (kf3 >= 3 * Kf) return;
     const int f = (int)(kf3 / Kf);
     const long kf = kf3 - f * Kf;
@@ -400,9 +417,9 @@ void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) 
     const int M = L->nn - 1;
     const int old = L->cur, nw = 1 - L->cur;
     const size_t bytes = 3 * L->K * sizeof(double2);
-    // node 0 keeps its right-hand sides (sdc.cpp:22-29: F_old is a copy; node 0 is not refreshed)
-    PSWE_CUDA(cudaMemcpyAsync(L->fi(0, nw), L->fi(0, old), bytes, cudaMemcpyDeviceToDevice, st));
-    PSWE_CUDA(cudaMemcpyAsync(L->fe(0, nw), L->fe(0, old), bytes, cudaMemcpyDeviceToDevice, st));
+    // node 0 keeps its right-hand sides (sdc.cpp:22-29: F_old is a copy; node 0 is not refreshed):
+    // the first node's update kernel copies them into the new buffer
+    (void)bytes;
     const Tables& t = L->tab;
     for (int m = 0; m < M; ++m) {
         SweepNodeArgs A{};
@@ -421,6 +438,8 @@ void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) 
             }
         }
         A.aii = dt * t.QI(m + 1, m + 1);
+        A.fi0_dst = m == 0 ? L->fi(0, nw) : nullptr;
+        A.fe0_dst = m == 0 ? L->fe(0, nw) : nullptr;
         A.m = m;
         A.M = M;
         A.R = L->R;
@@ -429,10 +448,9 @@ void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) 
         A.nu = L->prm.nu;
         const dim3 grid((unsigned)((L->K + 127) / 128)), block(128, 3);
         switch (L->nn) {
-            case 2: sweep_node_kernel<2><<<grid, block, 0, st>>>(A); break;
-            case 3: sweep_node_kernel<3><<<grid, block, 0, st>>>(A); break;
-            case 4: sweep_node_kernel<4><<<grid, block, 0, st>>>(A); break;
-            default: sweep_node_kernel<5><<<grid, block, 0, st>>>(A); break;
+            case 2: launch_pdl(sweep_node_kernel<2>, grid, block, 0, st, A); break;
+            case 3: launch_pdl(sweep_node_kernel<3>, grid, block, 0, st, A); break;
+            default: launch_pdl(sweep_node_kernel<5>, grid, block, 0, st, A); break;
         }
         PSWE_LAUNCH_CHECK();
         eval_imex(*L->plan, L->prm, L->st(m + 1), L->fi(m + 1, nw), L->fe(m + 1, nw), 1, st);
@@ -455,10 +473,9 @@ void level_residual(pswe_level* L, double dt, double* out, cudaStream_t st) {
     const unsigned g = (unsigned)((A.n3 + bs - 1) / bs);
     auto* o = reinterpret_cast<unsigned long long*>(out);
     switch (L->nn) {
-        case 2: residual_kernel<2><<<g, bs, 0, st>>>(A, o); break;
-        case 3: residual_kernel<3><<<g, bs, 0, st>>>(A, o); break;
-        case 4: residual_kernel<4><<<g, bs, 0, st>>>(A, o); break;
-        default: residual_kernel<5><<<g, bs, 0, st>>>(A, o); break;
+        case 2: launch_pdl(residual_kernel<2>, dim3(g), dim3(bs), 0, st, A, o); break;
+        case 3: launch_pdl(residual_kernel<3>, dim3(g), dim3(bs), 0, st, A, o); break;
+        default: launch_pdl(residual_kernel<5>, dim3(g), dim3(bs), 0, st, A, o); break;
     }
     PSWE_LAUNCH_CHECK();
 }
@@ -472,8 +489,8 @@ void pair_restrict_states(pswe_pair* P, cudaStream_t st) {
     for (int i = 0; i < C->nn; ++i)
         for (int j = 0; j < F->nn; ++j) A.w[i][j] = P->tr[(size_t)i * F->nn + j];
     const long n = 3 * C->K;
-    restrict_states_kernel<<<dim3((unsigned)((n + 127) / 128), C->nn), 128, 0, st>>>(A, C->st(0), 3 * C->K, F->R,
-                                                                                   C->R);
+    launch_pdl(restrict_states_kernel, dim3((unsigned)((n + 127) / 128), C->nn), dim3(128), 0, st, A, C->st(0),
+               3 * C->K, F->R, C->R);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -500,7 +517,7 @@ void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st, const doub
         for (int j = 0; j < C->nn; ++j) A.qc[i][j] = C->tab.Q(i, j);
     }
     const long n = 3 * C->K;
-    fas_kernel<<<dim3((unsigned)((n + 127) / 128), C->nn), 128, 0, st>>>(A, tau);
+    launch_pdl(fas_kernel, dim3((unsigned)((n + 127) / 128), C->nn), dim3(128), 0, st, A, tau);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -534,7 +551,7 @@ void pair_interp_increment_add(pswe_pair* P, double2* dstate0, cudaStream_t st) 
         for (int j = 0; j < C->nn; ++j) A.w[i][j] = P->ti[(size_t)i * C->nn + j];
     }
     const long n = 3 * F->K;
-    interp_kernel<<<dim3((unsigned)((n + 127) / 128), 3 * F->nn), 128, 0, st>>>(A, 0);
+    launch_pdl(interp_kernel, dim3((unsigned)((n + 127) / 128), 3 * F->nn), dim3(128), 0, st, A, 0);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -552,7 +569,7 @@ void pair_interp_states(pswe_pair* P, cudaStream_t st) {
         for (int j = 0; j < C->nn; ++j) A.w[i][j] = P->ti[(size_t)i * C->nn + j];
     }
     const long n = 3 * F->K;
-    interp_kernel<<<dim3((unsigned)((n + 127) / 128), F->nn), 128, 0, st>>>(A, 1);
+    launch_pdl(interp_kernel, dim3((unsigned)((n + 127) / 128), F->nn), dim3(128), 0, st, A, 1);
     PSWE_LAUNCH_CHECK();
 }
 
@@ -601,6 +618,8 @@ int pswe_quadrature_tables(int n, double* nodes, double* q, double* qe, double* 
 int pswe_level_create(pswe_plan* plan, const pswe_params* p, int num_nodes, pswe_level** out) {
     return guarded([&] {
         if (!plan || !p || !out) throw std::invalid_argument("pswe_level_create: NULL argument");
+        if (num_nodes != 2 && num_nodes != 3 && num_nodes != 5)  // the kernels' node arrays hold kMaxNodes
+            throw std::invalid_argument("pswe_level_create: supported node counts are 2, 3, 5");
         auto* L = new pswe_level;
         try {
             L->plan = plan;

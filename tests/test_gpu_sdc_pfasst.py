@@ -128,3 +128,12 @@ def test_pfasst_nccl_executor_single_rank(P, golden):
     assert rel_diff_fields(fin, golden["pf_nts1_final"]) < 1e-10
     assert res_ok(hist, golden["pf_nts1_res"], fin)
     pf.close()
+
+
+def test_level_rejects_unsupported_node_counts(P):
+    """Gauss-Lobatto tables exist for 2, 3, 5 nodes (sdc.cpp; the kernels size their node arrays
+    for at most 5): other counts are an error, not an out-of-bounds launch."""
+    plan = P.TransformPlan(15)
+    for nn in (1, 4, 6):
+        with pytest.raises(P._lib.PsweError):
+            P.Level(plan, P.ModelParams(), nn)
