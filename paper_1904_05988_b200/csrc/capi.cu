@@ -22,8 +22,9 @@ namespace pswe {
 // eval_implicit + eval_explicit of n states: the hot path (swe.cpp:9-69).
 // 4 launches: inverse Legendre (Phi, zeta, U, V) -> fused FFT/products/FFT -> forward Legendre
 // (5 projections) -> tail (tendency assembly + linear operator).
-void eval_imex(pswe_plan& P, const pswe_params& prm, const double2* state, double2* f_imp, double2* f_exp,
-               int n, cudaStream_t st) {
+// the evaluation up to the five projections in P.d_proj ([5n][Kx]); the tail (eval_tail, or the
+// SDC sweep's fused tail + node update) turns them into F_E / F_I
+void eval_imex_proj(pswe_plan& P, const pswe_params& prm, const double2* state, int n, cudaStream_t st) {
     P.reserve(n);
     legendre_inverse(P, INV_EVAL, state, nullptr, n, prm.radius, P.d_four_a, st);
     if (gt_path_ok(P, n)) {  // grid stage writes forward G tiles directly
@@ -33,6 +34,11 @@ void eval_imex(pswe_plan& P, const pswe_params& prm, const double2* state, doubl
         fft_eval_products(P, prm, P.d_four_a, P.d_four_b, n, st);
         legendre_forward(P, P.d_four_b, 5, n, P.d_proj, true, st);
     }
+}
+
+void eval_imex(pswe_plan& P, const pswe_params& prm, const double2* state, double2* f_imp, double2* f_exp,
+               int n, cudaStream_t st) {
+    eval_imex_proj(P, prm, state, n, st);
     eval_tail(P, prm, P.d_proj, state, f_imp, f_exp, n, st);
 }
 

@@ -1,6 +1,7 @@
 // Spectral-space elementwise / banded kernels (sm_100a, fp64): the tails of eval_nonlinear and
 // vortdiv_from_uv, eval_linear, solve_implicit, laplacian.
 #include "pswe_internal.h"
+#include "tail.cuh"
 
 namespace pswe {
 
@@ -8,41 +9,11 @@ namespace {
 
 __device__ __forceinline__ double2 cz() { return make_double2(0.0, 0.0); }
 
-// (r, s) of r-major index k (field.hpp:29-32)
-__device__ __forceinline__ void decode_rs(int R, long k, int& m, int& s) {
-    const double b = 2.0 * R + 3.0;
-    int mm = (int)floor((b - sqrt(b * b - 8.0 * (double)k)) * 0.5);
-    if (mm < 0) mm = 0;
-    if (mm > R) mm = R;
-    while (mm > 0 && off_std(R, mm) > k) --mm;
-    while (mm < R && off_std(R, mm + 1) <= k) ++mm;
-    m = mm;
-    s = mm + (int)(k - off_std(R, mm));
-}
+using tailc::decode_rs;
+using tailc::hcomb;
 
-// H-combination of a projection A (extended layout, block m): H_s = -s eps_{s+1} A_{s+1} + (s+1) eps_s A_{s-1}
-// (the lower neighbour's load is clamped rather than branched, so all loads issue together)
-__device__ __forceinline__ double2 hcomb(const double2* __restrict__ A, const double* __restrict__ eps, long bx,
-                                         int m, int s) {
-    const int t = s - m;
-    const double fu = -(double)s * eps[bx + t + 1];
-    const double2 up = A[bx + t + 1];
-    const double el = eps[bx + t];
-    const double2 lo = A[bx + (t > 0 ? t - 1 : 0)];
-    double2 h = make_double2(fu * up.x, fu * up.y);
-    if (t > 0) {
-        const double fl = (s + 1.0) * el;
-        h.x += fl * lo.x;
-        h.y += fl * lo.y;
-    }
-    return h;
-}
-
-// eval_nonlinear assembly (swe.cpp:61-67) from the five projections A1..A5 (extended layout,
-// s = m..R+1) plus eval_linear (swe.cpp:9-25) of the same state:
-//   Phi_t  = -(i m A1 - H[A2])          (-flux_div)
-//   zeta_t = -(i m A3 - H[A4])          (-q_div)
-//   div_t  = (i m A4 + H[A3]) - lap(A5) (q_curl - lap ke)
+// eval_nonlinear assembly (swe.cpp:61-67) plus eval_linear (swe.cpp:9-25) of the same state, one
+// thread per coefficient doing the three fields (tail.cuh: tail_field)
 __global__ void eval_tail_kernel(int R, const double* __restrict__ eps, const double2* __restrict__ proj,
                                  const double2* __restrict__ state, double2* __restrict__ f_imp,
                                  double2* __restrict__ f_exp, double inv_a2, double phi_bar, double nu) {
@@ -57,27 +28,16 @@ __global__ void eval_tail_kernel(int R, const double* __restrict__ eps, const do
     decode_rs(R, k, m, s);
     const long bx = off_ext(R, m);
     const double2* A = proj + (long)b * 5 * Kx;
-    const double2 a1 = A[bx + s - m], a3 = A[2 * Kx + bx + s - m], a4 = A[3 * Kx + bx + s - m];
-    const double2 a5 = A[4 * Kx + bx + s - m];
-    const double2 h2 = hcomb(A + Kx, eps, bx, m, s), h3 = hcomb(A + 2 * Kx, eps, bx, m, s);
-    const double2 h4 = hcomb(A + 3 * Kx, eps, bx, m, s);
     const double lam = -s * (s + 1.0) * inv_a2;
-    // flux_div = i m a1 - h2
-    const double2 fdiv = make_double2(-m * a1.y - h2.x, m * a1.x - h2.y);
-    const double2 qdiv = make_double2(-m * a3.y - h4.x, m * a3.x - h4.y);
-    const double2 qcurl = make_double2(-m * a4.y + h3.x, m * a4.x + h3.y);
-    const double2 kel = make_double2(lam * a5.x, lam * a5.y);
+    const double2* st = state + (long)b * 3 * K;
     double2* fe = f_exp + (long)b * 3 * K;
-    fe[k] = make_double2(-fdiv.x, -fdiv.y);
-    fe[K + k] = make_double2(-qdiv.x, -qdiv.y);
-    fe[2 * K + k] = make_double2(qcurl.x - kel.x, qcurl.y - kel.y);
-    if (f_imp) {
-        const double2* st = state + (long)b * 3 * K;
-        const double2 ph = st[k], vo = st[K + k], dv = st[2 * K + k];
-        double2* fi = f_imp + (long)b * 3 * K;
-        fi[k] = make_double2(-phi_bar * dv.x + nu * lam * ph.x, -phi_bar * dv.y + nu * lam * ph.y);
-        fi[K + k] = make_double2(nu * lam * vo.x, nu * lam * vo.y);
-        fi[2 * K + k] = make_double2(-lam * ph.x + nu * lam * dv.x, -lam * ph.y + nu * lam * dv.y);
+    double2* fi = f_imp ? f_imp + (long)b * 3 * K : nullptr;
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+        double2 e, i;
+        tailc::tail_field(f, eps, A, Kx, bx, m, s, lam, st, K, k, phi_bar, nu, fi != nullptr, e, i);
+        fe[f * K + k] = e;
+        if (fi) fi[f * K + k] = i;
     }
 }
 

@@ -15,10 +15,12 @@
 #include <cstring>
 
 #include "pswe_internal.h"
+#include "tail.cuh"
 
 namespace pswe {
 void eval_imex(pswe_plan& P, const pswe_params& prm, const double2* state, double2* f_imp, double2* f_exp, int n,
                cudaStream_t st);
+void eval_imex_proj(pswe_plan& P, const pswe_params& prm, const double2* state, int n, cudaStream_t st);
 
 // ---- quadrature tables (quadrature.cpp:19-106) ---------------------------------------------
 
@@ -113,6 +115,9 @@ struct SweepNodeArgs {
     double aii;                           // dt*qI(m+1,m+1)
     double2* fi0_dst;                     // node 0's F_I, F_E copied old -> new buffer (first node only)
     double2* fe0_dst;
+    const double2* proj;                  // fused tail: projections of state m ([5][Kx]), the state,
+    const double2* st_m;                  // and the degree recurrence eps
+    const double* eps;
     int m, M, R;
     double inv_a2, phi_bar, nu;
 };
@@ -149,23 +154,37 @@ __device__ __forceinline__ void decode(int R, long k, int& m, int& s) {
 // rhs (sdc.cpp:31-44, same axpy order) then solve_implicit (swe.cpp:77-98). Block (128, 3): thread
 // (x, f) accumulates field f of coefficient k (node loops unrolled over NN nodes, loads predicated on
 // j <= m so they all issue together); field 0's thread then solves the coupled (Phi, delta) system.
-template <int NN>
+// TAIL: the same kernel first finishes node m's evaluation (tail.cuh, the five projections of
+// state m in proj) and writes F_new[m], which the node-m+1 update then takes from registers -
+// one launch fewer per node, the same expressions as eval_tail + sweep_node (tail.cuh).
+template <int NN, bool TAIL>
 __global__ void __launch_bounds__(384) sweep_node_kernel(SweepNodeArgs A) {
     __shared__ double2 rs[3][128];
     const long K = (long)(A.R + 1) * (A.R + 2) / 2;
     const long k = (long)blockIdx.x * 128 + threadIdx.x;
     const int f = threadIdx.y;
     pdl_trigger();
-    pdl_wait();  // F and states come from the preceding evaluation
+    pdl_wait();  // F and states (TAIL: the projections) come from the preceding kernel
     if (k < K) {
         const long i = f * K + k;
+        double2 fe_m = make_double2(0.0, 0.0), fi_m = make_double2(0.0, 0.0);
+        if constexpr (TAIL) {
+            int mo, s;
+            tailc::decode_rs(A.R, k, mo, s);
+            const long Kx = (long)(A.R + 1) * (A.R + 4) / 2;
+            tailc::tail_field(f, A.eps, A.proj, Kx, off_ext(A.R, mo), mo, s, -s * (s + 1.0) * A.inv_a2,
+                              A.st_m, K, k, A.phi_bar, A.nu, true, fe_m, fi_m);
+            const_cast<double2*>(A.fe_new[A.m])[i] = fe_m;
+            const_cast<double2*>(A.fi_new[A.m])[i] = fi_m;
+        }
         double2 acc = A.theta0[i];
 #pragma unroll
         for (int j = 1; j < NN; ++j) {
             if (j <= A.m) {
-                axpy(acc, A.ae[j], A.fe_new[j][i]);
+                const bool reg = TAIL && j == A.m;
+                axpy(acc, A.ae[j], reg ? fe_m : A.fe_new[j][i]);
                 axpy(acc, -A.ae[j], A.fe_old[j][i]);
-                axpy(acc, A.ai[j], A.fi_new[j][i]);
+                axpy(acc, A.ai[j], reg ? fi_m : A.fi_new[j][i]);
                 axpy(acc, -A.ai[j], A.fi_old[j][i]);
             }
         }
@@ -447,14 +466,26 @@ void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) 
         A.phi_bar = L->prm.phi_bar;
         A.nu = L->prm.nu;
         const dim3 grid((unsigned)((L->K + 127) / 128)), block(128, 3);
-        switch (L->nn) {
-            case 2: launch_pdl(sweep_node_kernel<2>, grid, block, 0, st, A); break;
-            case 3: launch_pdl(sweep_node_kernel<3>, grid, block, 0, st, A); break;
-            default: launch_pdl(sweep_node_kernel<5>, grid, block, 0, st, A); break;
+        if (m > 0) {  // finish node m's evaluation in the same kernel
+            A.proj = L->plan->d_proj;
+            A.st_m = L->st(m);
+            A.eps = L->plan->d_eps;
+            switch (L->nn) {
+                case 2: launch_pdl(sweep_node_kernel<2, true>, grid, block, 0, st, A); break;
+                case 3: launch_pdl(sweep_node_kernel<3, true>, grid, block, 0, st, A); break;
+                default: launch_pdl(sweep_node_kernel<5, true>, grid, block, 0, st, A); break;
+            }
+        } else {
+            switch (L->nn) {
+                case 2: launch_pdl(sweep_node_kernel<2, false>, grid, block, 0, st, A); break;
+                case 3: launch_pdl(sweep_node_kernel<3, false>, grid, block, 0, st, A); break;
+                default: launch_pdl(sweep_node_kernel<5, false>, grid, block, 0, st, A); break;
+            }
         }
         PSWE_LAUNCH_CHECK();
-        eval_imex(*L->plan, L->prm, L->st(m + 1), L->fi(m + 1, nw), L->fe(m + 1, nw), 1, st);
+        eval_imex_proj(*L->plan, L->prm, L->st(m + 1), 1, st);
     }
+    eval_tail(*L->plan, L->prm, L->plan->d_proj, L->st(M), L->fi(M, nw), L->fe(M, nw), 1, st);
     L->cur = nw;
 }
 

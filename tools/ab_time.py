@@ -66,6 +66,19 @@ for R, nlat, nlon in ((255, 256, 512), (511, 512, 1024)):
             tt.append(a.elapsed_time(b) * 1e3)
     out[f"batch5_us_T{R}"] = round(float(np.median(tt)), 1)
     del plan
+# one fine SDC sweep (5 nodes: 4 single-state evaluations + node updates) and one coarse sweep
+for R, nlat, nlon, nn in ((255, 256, 512, 5), (127, 128, 256, 3)):
+    lvl = P.Level(P.TransformPlan(R, nlat, nlon), prm, nn)
+    lvl.spread(torch.as_tensor(balanced_random_state(R, 40.0, 3)).cuda())
+    for _ in range(5):
+        lvl.sweep(60.0)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(50):
+        lvl.sweep(60.0)
+    b.record()
+    torch.cuda.synchronize()
+    out[f"sweep_us_T{R}_{nn}"] = round(a.elapsed_time(b) * 1e3 / 50, 1)
 dev = torch.device("cuda:0")
 for c in configs:
     r = bench.run_pfasst(P, prm, 1, 0, dev, config=c)
