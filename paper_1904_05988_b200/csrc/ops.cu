@@ -32,12 +32,14 @@ __global__ void eval_tail_kernel(int R, const double* __restrict__ eps, const do
     const double2* st = state + (long)b * 3 * K;
     double2* fe = f_exp + (long)b * 3 * K;
     double2* fi = f_imp ? f_imp + (long)b * 3 * K : nullptr;
+    double2 e[3], i[3];  // every load before any store
+#pragma unroll
+    for (int f = 0; f < 3; ++f)
+        tailc::tail_field(f, eps, A, Kx, bx, m, s, lam, st, K, k, phi_bar, nu, fi != nullptr, e[f], i[f]);
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
-        double2 e, i;
-        tailc::tail_field(f, eps, A, Kx, bx, m, s, lam, st, K, k, phi_bar, nu, fi != nullptr, e, i);
-        fe[f * K + k] = e;
-        if (fi) fi[f * K + k] = i;
+        fe[f * K + k] = e[f];
+        if (fi) fi[f * K + k] = i[f];
     }
 }
 
