@@ -73,10 +73,14 @@ __host__ __device__ constexpr int ip_off(int N, int s) {  // twiddle table offse
 }
 
 // blocks per SM the register budget is sized for: 4 (64 registers) when every radix is <= 8,
-// fewer for the radix-12/16 plans (their butterflies alone hold 24-32 doubles)
+// fewer for the radix-12/16 plans (their butterflies alone hold 24-32 doubles). N = 256 (T255 on
+// 256 x 512): 3 (78 registers) - the single-state evaluation of an SDC sweep has one block per
+// latitude (256 < 3 x 148), so fewer instructions per block win (eval 36.3 -> 34.0 us, fine sweep
+// 177 -> 166 us; the 5-state batch is unchanged); at N = 512 the same change costs 2 us.
 __host__ __device__ constexpr int ip_minblocks(int N) {
     int mx = 0;
     for (int s = 0; ip_radix(N, s); ++s) mx = ip_radix(N, s) > mx ? ip_radix(N, s) : mx;
+    if (mx <= 8 && N == 256) return 3;
     if (mx <= 8) return N <= 512 ? 4 : 2;
     return N <= 1024 ? 2 : 1;
 }
@@ -209,8 +213,13 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
         xa[u] = xb[u] = make_double2(0.0, 0.0);
         const int f = it / HS, k = it - f * HS;
         if (f < 4 && k < H) {
+#ifdef PSWE_FDIAG_NOLOAD
+            xa[u] = make_double2(1.0 + k, 0.5 * f);
+            xb[u] = make_double2(0.25 * k, 1.0);
+#else
             if (k <= R) xa[u] = in[f * rowsz + k];
             if (k > 0 && N - k <= R) xb[u] = in[f * rowsz + N - k];
+#endif
         }
     }
 #pragma unroll
@@ -286,6 +295,10 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
             const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);
             const double2 x = cadd(e, cmul(w, o));
             const double sc = q < 4 ? sflux : ske;
+#ifdef PSWE_FDIAG_NOSTORE
+            if (x.x == 1.2345e300) gt[0] = x.y;
+            continue;
+#endif
             if constexpr (GT) {
                 double* d = gt + k * gstep + ((gcol + 2 * q) ^ swz);
                 *reinterpret_cast<double2*>(d) = make_double2(x.x * sc, x.y * sc);
