@@ -237,8 +237,13 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
 // bulk copy of the G tile of each order (both hemispheres, written in this layout by the grid
 // stage) and one 1 KB copy per chunk of the P table, into an S-stage mbarrier ring.
 // G_E = G_N + G_S and G_O = G_N - G_S are formed in registers and reused by the CPW chunks.
+// register budget: the 8-warp and the narrow (one / two state, 32-latitude stage) configurations
+// are held to 2 blocks per SM by shared memory anyway; saying so lets ptxas use 72-118 registers
+// instead of its own 48-64 (+spills): single-state forward T255 -1.1 us, T511 -6 us. The 4-warp
+// wide configurations keep ptxas' default (0 = unspecified; an explicit 1 or 2 grows the T511
+// tiling to 188 registers and loses 6%).
 template <int NTC, int W, int CPW, int S, int SUB>
-__global__ void __launch_bounds__(32 * W) leg_fwd_gt_kernel(int R, int Jp, int nq, GtLayout gl,
+__global__ void __launch_bounds__(32 * W, (W == 8 || SUB == 4) ? 2 : 0) leg_fwd_gt_kernel(int R, int Jp, int nq, GtLayout gl,
                                                            const double* __restrict__ ptab,
                                                            const int* __restrict__ cbase,
                                                            const int4* __restrict__ tasks_a,
