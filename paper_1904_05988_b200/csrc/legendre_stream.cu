@@ -693,8 +693,10 @@ void fwd_launch(const pswe_plan& P, const double2* four, int nq, double2* out, b
 #ifndef PSWE_INV_STAGES
 #define PSWE_INV_STAGES 4
 #endif
+// one latitude slice (two warps, 64 threads) per block: measured -2% on the T255 5-state batch
+// and -1.3% at T511 against two slices (four: +1-3%); the X tile is re-read per slice from L2
 #ifndef PSWE_INV_SLICES
-#define PSWE_INV_SLICES 2
+#define PSWE_INV_SLICES 1
 #endif
 constexpr int kInvStages = PSWE_INV_STAGES;  // ring stages (one chunk each)
 constexpr int kInvSlices = PSWE_INV_SLICES;  // latitude slices per block (two warps each)
