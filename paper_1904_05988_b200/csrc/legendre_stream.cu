@@ -701,15 +701,18 @@ void fwd_launch(const pswe_plan& P, const double2* four, int nq, double2* out, b
 constexpr int kInvStages = PSWE_INV_STAGES;  // ring stages (one chunk each)
 constexpr int kInvSlices = PSWE_INV_SLICES;  // latitude slices per block (two warps each)
 
-// column tiles per group for nq complex columns. Measured for the TMA kernel
-// (tools/stage_times.py, 5-state batch, 20 columns): NT = 2 at 128 latitude pairs (40.0 us vs 45-47
-// for NT = 1, 4, 5), NT = 3 at 192 (51.9 vs 54-59): small NT keeps registers low (more resident
-// warps) and gives more, better-balanced blocks; the extra P re-reads hit L2. One tile for <= 4
-// columns. PSWE_INV_NT overrides (tuning only).
-int inv_choose_nt(const pswe_plan& P, int nq) {
+// column tiles per group for nq complex columns. With one latitude slice per block (r01f,
+// tools/ab_time.py): evaluation batches of up to 5 states take all their columns in one group
+// (the P table streams once; 5 states: T255 103.5 -> 102.3 us, T511 503 -> 479 us against 2 / 3
+// tiles). Other inputs (the plain transforms' fields) keep small groups: NT = 2 below 192 latitude
+// pairs, 3 from 192 (15 fields at T255: NT = 2 46 us, 3-5 48-50 us) - small NT keeps registers
+// low and gives more blocks; the P re-reads hit L2. One tile for <= 4 columns. PSWE_INV_NT
+// overrides (tuning only).
+int inv_choose_nt(const pswe_plan& P, int nq, int kind) {
     static const int forced = [] { const char* e = getenv("PSWE_INV_NT"); return e ? atoi(e) : 0; }();
     if (forced >= 1 && forced <= 5) return forced;
     if (nq <= 4) return 1;
+    if (kind == INV_EVAL && nq <= 20) return (nq + 3) / 4;
     return P.J >= 192 ? 3 : 2;
 }
 
@@ -878,7 +881,7 @@ void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, do
 void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq,
                              double radius, double2* out, cudaStream_t st, cudaEvent_t after_prep) {
     if (nq <= 0) return;
-    const int NT = inv_choose_nt(P, nq);
+    const int NT = inv_choose_nt(P, nq, kind);
     const int NQ = 4 * NT, SX = 8 * NT + 2;
     const int groups = (nq + NQ - 1) / NQ;
     const size_t need = (size_t)groups * P.n_chunks * CH * SX;
