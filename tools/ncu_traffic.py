@@ -21,7 +21,8 @@ def main():
     def val(r, k):
         v = float(r[hdr.index(k)].replace(",", ""))
         u = units[hdr.index(k)]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "ns": 1e-9,
+                 "us": 1e-6, "ms": 1e-3,
                  "msecond": 1e-3}.get(u, 1)
         return v * scale
 
