@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
     }
     for (int k = threadIdx.x; k <= R; k += kIpThreads) {
         const double2 w = __ldg(post + k);
+        double v[10];  // the 5 scaled X_k, (re, im) each
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
             const double2 zk = A[ipad(q * N + k)];
@@ -295,17 +296,44 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
             const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);
             const double2 x = cadd(e, cmul(w, o));
             const double sc = q < 4 ? sflux : ske;
+            v[2 * q] = x.x * sc;
+            v[2 * q + 1] = x.y * sc;
+        }
 #ifdef PSWE_FDIAG_NOSTORE
-            if (x.x == 1.2345e300) gt[0] = x.y;
-            continue;
+        if (v[0] == 1.2345e300) gt[0] = v[1];
+        continue;
 #endif
-            if constexpr (GT) {
-                double* d = gt + k * gstep + ((gcol + 2 * q) ^ swz);
-                *reinterpret_cast<double2*>(d) = make_double2(x.x * sc, x.y * sc);
-                if (equator) *reinterpret_cast<double2*>(d + 8 * gl.sgc) = make_double2(0.0, 0.0);  // G_S := 0
+        if constexpr (GT) {
+            // the state's 10 columns gcol.. of this row: the XOR swizzle (a multiple of 4) maps
+            // 4-aligned column groups onto 4-aligned groups, so they go out as two 32-byte stores
+            // and one 16-byte store (gcol = 10 b is 0 or 2 mod 4)
+            double* row = gt + k * gstep;
+            auto st4 = [&](int c, double a0, double a1, double a2, double a3) {
+                double* p4 = row + (c ^ swz);
+                asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(p4), "d"(a0), "d"(a1), "d"(a2),
+                             "d"(a3)
+                             : "memory");
+                if (equator)  // G_S := 0
+                    asm volatile("st.global.v4.f64 [%0], {%1, %1, %1, %1};\n" ::"l"(p4 + 8 * gl.sgc), "d"(0.0)
+                                 : "memory");
+            };
+            auto st2 = [&](int c, double a0, double a1) {
+                double* p2 = row + (c ^ swz);
+                *reinterpret_cast<double2*>(p2) = make_double2(a0, a1);
+                if (equator) *reinterpret_cast<double2*>(p2 + 8 * gl.sgc) = make_double2(0.0, 0.0);
+            };
+            if ((gcol & 3) == 0) {
+                st4(gcol, v[0], v[1], v[2], v[3]);
+                st4(gcol + 4, v[4], v[5], v[6], v[7]);
+                st2(gcol + 8, v[8], v[9]);
             } else {
-                out[q * rowsz + (long)k * nlat] = make_double2(x.x * sc, x.y * sc);
+                st2(gcol, v[0], v[1]);
+                st4(gcol + 2, v[2], v[3], v[4], v[5]);
+                st4(gcol + 6, v[6], v[7], v[8], v[9]);
             }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 5; ++q) out[q * rowsz + (long)k * nlat] = make_double2(v[2 * q], v[2 * q + 1]);
         }
     }
 }
