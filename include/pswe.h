@@ -112,6 +112,7 @@ int pswe_eval_imex_kernel_times(pswe_plan* plan, const pswe_params* p, const dou
                                 double* f_exp, int n_states, void* stream, float* ms_out);
 
 /* ---- SDC level: LevelSpec + SpaceTimeState on the device (sdc.hpp:14-45) */
+/* num_nodes: 2, 3 or 5 Gauss-Lobatto nodes (quadrature.cpp); any other count is an error */
 int pswe_level_create(pswe_plan* plan, const pswe_params* p, int num_nodes, pswe_level** out);
 int pswe_level_destroy(pswe_level* lvl);
 /* which: 0 = state, 1 = f_imp, 2 = f_exp; returns the device pointer of that node's 3K complex */

@@ -106,9 +106,9 @@ struct SweepNodeArgs {
     const double2* theta0;
     const double2* tau;  // tau[m+1] or nullptr
     double2* out;
-    const double2* fe_new[kMaxNodes];
+    double2* fe_new[kMaxNodes];  // written at node m by the fused tail
     const double2* fe_old[kMaxNodes];
-    const double2* fi_new[kMaxNodes];
+    double2* fi_new[kMaxNodes];
     const double2* fi_old[kMaxNodes];
     double ae[kMaxNodes], ai[kMaxNodes];  // dt*qE(m+1,j), dt*qI(m+1,j), j = 1..m
     double aq[kMaxNodes];                 // dt*q(m+1,j), j = 0..M
@@ -174,8 +174,8 @@ __global__ void __launch_bounds__(384) sweep_node_kernel(SweepNodeArgs A) {
             const long Kx = (long)(A.R + 1) * (A.R + 4) / 2;
             tailc::tail_field(f, A.eps, A.proj, Kx, off_ext(A.R, mo), mo, s, -s * (s + 1.0) * A.inv_a2,
                               A.st_m, K, k, A.phi_bar, A.nu, true, fe_m, fi_m);
-            const_cast<double2*>(A.fe_new[A.m])[i] = fe_m;
-            const_cast<double2*>(A.fi_new[A.m])[i] = fi_m;
+            A.fe_new[A.m][i] = fe_m;
+            A.fi_new[A.m][i] = fi_m;
         }
         double2 acc = A.theta0[i];
 #pragma unroll
