@@ -242,8 +242,14 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
 // instead of its own 48-64 (+spills): single-state forward T255 -1.1 us, T511 -6 us. The 4-warp
 // wide configurations keep ptxas' default (0 = unspecified; an explicit 1 or 2 grows the T511
 // tiling to 188 registers and loses 6%).
-template <int NTC, int W, int CPW, int S, int SUB>
-__global__ void __launch_bounds__(32 * W, (W == 8 || SUB == 4) ? 2 : 0) leg_fwd_gt_kernel(int R, int Jp, int nq, GtLayout gl,
+// PROD: one extra warp only issues the ring refills (it waits for the compute warps' release of
+// stage q and issues stage q + S), so no compute warp stalls on the slowest one before its next
+// stage (T255 batch 98.3 -> 96.8 us, T511 batch 461 -> 443 us). PSWE_FWD_PROD=0: warp 0 refills.
+#ifndef PSWE_FWD_PROD
+#define PSWE_FWD_PROD 1
+#endif
+template <int NTC, int W, int CPW, int S, int SUB, bool PROD = PSWE_FWD_PROD>
+__global__ void __launch_bounds__(32 * (W + (PROD ? 1 : 0)), (W == 8 || SUB == 4) ? 2 : 0) leg_fwd_gt_kernel(int R, int Jp, int nq, GtLayout gl,
                                                            const double* __restrict__ ptab,
                                                            const int* __restrict__ cbase,
                                                            const int4* __restrict__ tasks_a,
@@ -332,6 +338,14 @@ __global__ void __launch_bounds__(32 * W, (W == 8 || SUB == 4) ? 2 : 0) leg_fwd_
     if (threadIdx.x == 0)
         for (int q = 0; q < S && q < nst; ++q) issue_g(q);
 
+    if (PROD && warp == W) {  // producer warp: ring refills only
+        if (lane == 0)
+            for (int q = 0; q + S < nst; ++q) {
+                mbar_wait(empty + q % S, (unsigned)(q / S) & 1u);
+                issue(q + S);
+            }
+        return;
+    }
     double acc[NTC][CPW][2][2];
 #pragma unroll
     for (int a = 0; a < NTC; ++a)
@@ -377,7 +391,7 @@ __global__ void __launch_bounds__(32 * W, (W == 8 || SUB == 4) ? 2 : 0) leg_fwd_
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + k);
-        if (threadIdx.x == 0 && q + S < nst) {
+        if (!PROD && threadIdx.x == 0 && q + S < nst) {
             mbar_wait(empty + k, ph);
             issue(q + S);
         }
@@ -419,7 +433,8 @@ void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out,
         PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         attr = (int)sm;
     }
-    launch_pdl(kern, dim3(P.n_fwd_tasks, gl.groups), dim3(32 * W), sm, st, P.R, Jp, nq, gl, P.d_ptab2, P.d_chk_off,
+    launch_pdl(kern, dim3(P.n_fwd_tasks, gl.groups), dim3(32 * (W + (PSWE_FWD_PROD ? 1 : 0))), sm, st, P.R, Jp, nq, gl,
+               P.d_ptab2, P.d_chk_off,
                P.d_fwd_ta, P.d_fwd_tb, P.d_gtile, out);
     PSWE_LAUNCH_CHECK();
 }
