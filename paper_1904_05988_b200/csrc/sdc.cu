@@ -129,26 +129,12 @@ __device__ __forceinline__ void axpy(double2& acc, double a, double2 x) {
     acc.y += a * x.y;
 }
 
+// (r, s) of r-major index k (field.hpp:29-32)
+using tailc::decode_rs;
 __device__ __forceinline__ int degree_of(int R, long k) {
-    const double b = 2.0 * R + 3.0;
-    int mm = (int)floor((b - sqrt(b * b - 8.0 * (double)k)) * 0.5);
-    if (mm < 0) mm = 0;
-    if (mm > R) mm = R;
-    while (mm > 0 && off_std(R, mm) > k) --mm;
-    while (mm < R && off_std(R, mm + 1) <= k) ++mm;
-    return mm + (int)(k - off_std(R, mm));
-}
-
-__device__ __forceinline__ void decode(int R, long k, int& m, int& s) {
-    s = degree_of(R, k);
-    const double b = 2.0 * R + 3.0;
-    int mm = (int)floor((b - sqrt(b * b - 8.0 * (double)k)) * 0.5);
-    if (mm < 0) mm = 0;
-    if (mm > R) mm = R;
-    while (mm > 0 && off_std(R, mm) > k) --mm;
-    while (mm < R && off_std(R, mm + 1) <= k) ++mm;
-    m = mm;
-    s = mm + (int)(k - off_std(R, mm));
+    int m, s;
+    decode_rs(R, k, m, s);
+    return s;
 }
 
 // rhs (sdc.cpp:31-44, same axpy order) then solve_implicit (swe.cpp:77-98). Block (128, 3): thread
@@ -276,7 +262,7 @@ __device__ __forceinline__ long fine_index(int Rf, int Rc, long kc3, long Kc, lo
     const int f = (int)(kc3 / Kc);
     const long kc = kc3 - f * Kc;
     int m, s;
-    decode(Rc, kc, m, s);
+    decode_rs(Rc, kc, m, s);
     return f * Kf + off_std(Rf, m) + (s - m);
 }
 
@@ -379,7 +365,7 @@ __global__ void interp_kernel(InterpArgs A, int mode) {
     const int f = (int)(kf3 / Kf);
     const long kf = kf3 - f * Kf;
     int m, s;
-    decode(A.Rf, kf, m, s);
+    decode_rs(A.Rf, kf, m, s);
     const bool inside = (m <= A.Rc && s <= A.Rc);
     double2 acc = make_double2(0.0, 0.0);
     if (inside) {
@@ -617,7 +603,7 @@ __global__ void space_copy_kernel(int Rf, int Rc, const double2* __restrict__ x,
         if (kf3 >= 3 * Kf) return;
         const int f = (int)(kf3 / Kf);
         int m, s;
-        decode(Rf, kf3 - f * Kf, m, s);
+        tailc::decode_rs(Rf, kf3 - f * Kf, m, s);
         y[b * 3 * Kf + kf3] = (m <= Rc && s <= Rc) ? x[b * 3 * Kc + f * Kc + off_std(Rc, m) + (s - m)]
                                                    : make_double2(0.0, 0.0);
     }
