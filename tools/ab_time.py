@@ -65,6 +65,13 @@ for R, nlat, nlon in ((255, 256, 512), (511, 512, 1024)):
         if it >= 5:
             tt.append(a.elapsed_time(b) * 1e3)
     out[f"batch5_us_T{R}"] = round(float(np.median(tt)), 1)
+    ks = []
+    for _ in range(30):
+        _lib.check(L.pswe_eval_imex_kernel_times(plan.handle, ctypes.byref(cp), st5.data_ptr(), fi5.data_ptr(),
+                                                 fe5.data_ptr(), 5, _stream(), ms))
+        ks.append(list(ms))
+    out[f"stages5_us_T{R}"] = dict(zip(("prep", "inverse", "fft", "forward", "tail"),
+                                       (round(float(v) * 1e3, 1) for v in np.median(np.array(ks), axis=0))))
     del plan
 # one fine SDC sweep (5 nodes: 4 single-state evaluations + node updates) and one coarse sweep
 for R, nlat, nlon, nn in ((255, 256, 512, 5), (127, 128, 256, 3)):
