@@ -92,6 +92,29 @@ def reference_eval_rate(seconds: float, threads: int | None = None):
     return n / el, cores, f"{n} sequential eval_nonlinear+eval_linear calls at T255 {NLAT}x{NLON} ({el:.1f} s)"
 
 
+def reference_pfasst(n_ts: int, theta0=None, config: int = 3):
+    """The reference's own pf::run_block (oracle/_ref, pfasst.cpp:194-251) on a BASELINE PFASST
+    config at n_ts time steps per block, ONE block timed (its steady_clock around run_block):
+    serial emulation with OpenMP on every host core at n_ts = 1, the reference's threaded mode
+    (one core per worker, pfasst.cpp:224) beyond — SURVEY §8d(4). Wall s per simulated day =
+    wall / (n_ts dt) * 86400. Two-level configs only (config 5's T1023 plan needs ~13 GB of host
+    memory and minutes per block; config 4 has no reference implementation)."""
+    from oracle import ref_lib as ref
+    from oracle.pswe_oracle import ModelParams
+    from paper_1904_05988_b200.cases import config_state
+    lv, dt, _, n_iter = PF_CONFIGS[config]
+    (Rf, nf_lat, nf_lon, nn_f), (Rc, nc_lat, nc_lon, nn_c) = lv
+    th = config_state(config) if theta0 is None else theta0
+    p = ModelParams(phi_bar=9.80616 * 1e4)
+    r = ref.pfasst_run(Rf, (nf_lat, nf_lon), Rc, (nc_lat, nc_lon), p, nn_f, nn_c, n_ts, dt, n_iter, 1, th,
+                       serial=(n_ts == 1))
+    cores = ref.lib().ref_max_threads()
+    return {"config": config, "n_ts": n_ts, "wall_s_per_sim_day": r.wall / (n_ts * dt) * 86400,
+            "wall_s": r.wall, "blocks": 1, "cores": cores if n_ts == 1 else n_ts, "kind": "reference",
+            "mode": "serial emulation, OpenMP" if n_ts == 1 else "threaded (one core per worker)",
+            "sample": f"one block of {n_ts} step(s), {n_iter} iterations (oracle/_ref pf::run_block)"}
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -131,6 +154,12 @@ def run_reference_arm(args):
                                    f"(OpenMP {cores} threads, FFTW-API shim)"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_pfasst:
+        try:  # the metric's second half: PFASST-SH wall s per simulated day (IC without the bump:
+            # the reference arm never touches the GPU; run time does not depend on the values)
+            line["pfasst"] = reference_pfasst(world)
+        except Exception as e:
+            line["pfasst"] = {"error": f"{type(e).__name__}: {e}"}
     print(json.dumps(line))
 
 
@@ -436,6 +465,14 @@ def run_ours(args):
             except Exception as e:  # reported, never hides the headline
                 pf_all[str(c)] = {"error": f"{type(e).__name__}: {e}"}
         pf_res = pf_all.get("3")
+        if rank == 0 and not args.no_cpu_baseline and pf_res is not None and "error" not in pf_res:
+            try:  # the reference's PFASST on the host cores, same IC and n_ts (outside the timed spans)
+                th = pf_res.pop("_theta0", None)
+                pf_res["cpu_reference"] = reference_pfasst(world, th)
+            except Exception as e:
+                pf_res["cpu_reference"] = {"error": f"{type(e).__name__}: {e}"}
+        for v in pf_all.values():
+            v.pop("_theta0", None)
 
     clk = clocks.stop()
 
@@ -524,7 +561,8 @@ def run_pfasst(P, prm, world, rank, dev, clocks_dev=0, config=3):
     return {"config": f"config {config}: {desc}, {nodes} nodes, dt {dt:g} s, {steps} steps, {n_iter} iterations",
             "levels": len(lv), "n_ts": world, "blocks": n_blocks, "wall_s": wall,
             "wall_s_per_sim_day": wall / (steps * dt) * 86400,
-            "final_residuals": [float(r) for r in hist[-1][:, -1]]}
+            "final_residuals": [float(r) for r in hist[-1][:, -1]],
+            "_theta0": theta0.cpu().numpy() if config == 3 else None}
 
 
 def main():
