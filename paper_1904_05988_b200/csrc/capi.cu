@@ -9,6 +9,10 @@ namespace {
 void need(const void* p, const char* what) {
     if (!p) throw std::invalid_argument(std::string(what) + " is NULL");
 }
+// data pointers of a batch of n: an empty batch (n <= 0) is a no-op and may pass NULL
+void need(const void* p, const char* what, int n) {
+    if (n > 0 && !p) throw std::invalid_argument(std::string(what) + " is NULL");
+}
 
 inline const double2* c2(const double* p) { return reinterpret_cast<const double2*>(p); }
 inline double2* c2(double* p) { return reinterpret_cast<double2*>(p); }
@@ -68,8 +72,8 @@ int pswe_stream_synchronize(void* stream) {
 int pswe_synthesise(pswe_plan* P, const double* coeffs, double* grid, int n, void* stream) {
     return guarded([&] {
         need(P, "plan");
-        need(coeffs, "coeffs");
-        need(grid, "grid");
+        need(coeffs, "coeffs", n);
+        need(grid, "grid", n);
         if (n <= 0) return;
         P->reserve(batch_groups(n, 5));
         legendre_inverse(*P, INV_PLAIN, c2(coeffs), nullptr, n, 1.0, P->d_four_a, as_stream(stream));
@@ -80,8 +84,8 @@ int pswe_synthesise(pswe_plan* P, const double* coeffs, double* grid, int n, voi
 int pswe_analyse(pswe_plan* P, const double* grid, double* coeffs, int n, void* stream) {
     return guarded([&] {
         need(P, "plan");
-        need(coeffs, "coeffs");
-        need(grid, "grid");
+        need(coeffs, "coeffs", n);
+        need(grid, "grid", n);
         if (n <= 0) return;
         P->reserve(batch_groups(n, 5));
         fft_rows_r2c(*P, grid, P->d_four_a, 1, 0, n, false, 0, 1.0, as_stream(stream));
@@ -93,10 +97,10 @@ int pswe_uv_from_vortdiv(pswe_plan* P, const double* vort, const double* div, do
                          double* v, int n, void* stream) {
     return guarded([&] {
         need(P, "plan");
-        need(vort, "vort");
-        need(div, "div");
-        need(u, "u");
-        need(v, "v");
+        need(vort, "vort", n);
+        need(div, "div", n);
+        need(u, "u", n);
+        need(v, "v", n);
         if (n <= 0) return;
         P->reserve(batch_groups(2 * n, 5));
         const cudaStream_t st = as_stream(stream);
@@ -110,10 +114,10 @@ int pswe_vortdiv_from_uv(pswe_plan* P, const double* u, const double* v, double 
                          double* div, int n, void* stream) {
     return guarded([&] {
         need(P, "plan");
-        need(vort, "vort");
-        need(div, "div");
-        need(u, "u");
-        need(v, "v");
+        need(vort, "vort", n);
+        need(div, "div", n);
+        need(u, "u", n);
+        need(v, "v", n);
         if (n <= 0) return;
         P->reserve(batch_groups(2 * n, 5));
         const cudaStream_t st = as_stream(stream);
@@ -126,8 +130,8 @@ int pswe_vortdiv_from_uv(pswe_plan* P, const double* u, const double* v, double 
 
 int pswe_laplacian(int R, const double* x, double radius, double* y, int n, int inverse, void* stream) {
     return guarded([&] {
-        need(x, "x");
-        need(y, "y");
+        need(x, "x", n);
+        need(y, "y", n);
         if (R < 1) throw std::invalid_argument("laplacian: truncation must be >= 1");
         laplacian(R, c2(x), radius, c2(y), n, inverse != 0, as_stream(stream));
     });
@@ -138,8 +142,8 @@ int pswe_eval_explicit(pswe_plan* P, const pswe_params* p, const double* state, 
     return guarded([&] {
         need(P, "plan");
         need(p, "params");
-        need(state, "state");
-        need(f_exp, "f_exp");
+        need(state, "state", n);
+        need(f_exp, "f_exp", n);
         if (n <= 0) return;
         eval_imex(*P, *p, c2(state), nullptr, c2(f_exp), n, as_stream(stream));
     });
@@ -148,8 +152,8 @@ int pswe_eval_explicit(pswe_plan* P, const pswe_params* p, const double* state, 
 int pswe_eval_implicit(int R, const pswe_params* p, const double* state, double* f_imp, int n, void* stream) {
     return guarded([&] {
         need(p, "params");
-        need(state, "state");
-        need(f_imp, "f_imp");
+        need(state, "state", n);
+        need(f_imp, "f_imp", n);
         if (R < 1) throw std::invalid_argument("eval_implicit: truncation must be >= 1");
         eval_linear(R, *p, c2(state), c2(f_imp), n, as_stream(stream));
     });
@@ -160,9 +164,9 @@ int pswe_eval_imex(pswe_plan* P, const pswe_params* p, const double* state, doub
     return guarded([&] {
         need(P, "plan");
         need(p, "params");
-        need(state, "state");
-        need(f_imp, "f_imp");
-        need(f_exp, "f_exp");
+        need(state, "state", n);
+        need(f_imp, "f_imp", n);
+        need(f_exp, "f_exp", n);
         if (n <= 0) return;
         eval_imex(*P, *p, c2(state), c2(f_imp), c2(f_exp), n, as_stream(stream));
     });
@@ -238,8 +242,8 @@ int pswe_eval_imex_kernel_times(pswe_plan* P, const pswe_params* p, const double
 int pswe_solve_implicit(int R, const pswe_params* p, const double* b, double c, double* out, int n, void* stream) {
     return guarded([&] {
         need(p, "params");
-        need(b, "b");
-        need(out, "out");
+        need(b, "b", n);
+        need(out, "out", n);
         if (R < 1) throw std::invalid_argument("solve_implicit: truncation must be >= 1");
         solve_implicit(R, *p, c2(b), c, c2(out), n, as_stream(stream));
     });

@@ -176,3 +176,39 @@ def test_zonal_jet_is_balanced(P):
     # Phi and zeta tendencies vanish for any zonal flow; the divergence tendency is the balance
     assert t_bal[2] < 3e-2 * t_unb[2]
     assert t_bal[0] < 1e-6 * p.phi_bar and t_bal[1] < 1e-12
+
+
+@pytest.mark.parametrize("R,grid,n", [(21, (45, 96), 1), (21, (45, 96), 3), (31, (49, 96), 5)])
+def test_eval_odd_latitudes_vs_oracle(P, R, grid, n):
+    """Odd latitude counts: the equator row is its own mirror (its G tile takes G_S := 0 in the
+    fused grid stage) and the last 32-latitude P/G slices are partly padding; single states and
+    batches against the numpy oracle's eval_nonlinear / eval_linear."""
+    from paper_1904_05988_b200.cases import balanced_random_state
+    plan = P.TransformPlan(R, grid[0], grid[1])
+    ref = O.TransformPlan(R, grid[0], grid[1])
+    p = P.ModelParams(phi_bar=9.80616 * 1e4, nu=1e5)
+    po = O.ModelParams(phi_bar=p.phi_bar, nu=1e5)
+    sts = np.stack([balanced_random_state(R, 30.0, 500 + s, phi_bar=p.phi_bar) for s in range(n)])
+    fi, fe = (host(t) for t in P.imex_split(cuda(sts), p, plan))
+    for i in range(n):
+        assert rel_diff_fields(fe[i], O.eval_nonlinear(sts[i], po, ref)) < 1e-11
+        assert rel_diff_fields(fi[i], O.eval_linear(R, sts[i], po)) < 1e-14
+
+
+def test_empty_batches(P):
+    """A batch of zero states / fields is a no-op (the reference's loops simply do not run): every
+    operator returns an empty result without launching or failing."""
+    R = 31
+    plan = P.TransformPlan(R)
+    p = P.ModelParams()
+    K = P.num_coeffs(R)
+    empty = torch.empty((0, 3, K), dtype=torch.complex128, device="cuda")
+    fi, fe = P.imex_split(empty, p, plan)
+    assert fi.shape == (0, 3, K) and fe.shape == (0, 3, K)
+    assert P.eval_nonlinear(empty, p, plan).shape == (0, 3, K)
+    assert P.eval_linear(R, empty, p).shape == (0, 3, K)
+    assert P.solve_implicit(R, empty, 60.0, p).shape == (0, 3, K)
+    g = plan.synthesise(torch.empty((0, K), dtype=torch.complex128, device="cuda"))
+    assert g.shape[0] == 0
+    assert plan.analyse(g).shape[0] == 0
+    torch.cuda.synchronize()
