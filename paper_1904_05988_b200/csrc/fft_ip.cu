@@ -178,6 +178,26 @@ __device__ __forceinline__ double2 c2r_z(double2 a, double2 bb, double2 w) {
     return make_double2(e.x - o.y, e.y + o.x);
 }
 
+// Latitude rows J .. 8 ns8 - 1 of a G tile are padding (the P table is zero there). The buffer is
+// shared by every batch size, each with its own layout, so those rows may hold another layout's
+// values; NaN/Inf there would survive the multiplication by zero. The producer of
+// row J - 1 of hemisphere h (one block per hemisphere) zeroes the padding rows of its ncol columns.
+__device__ void gt_zero_pad(double* __restrict__ gtile, const GtLayout& gl, int R, int J, int z, int h, int gcol,
+                            int ncol, int nthreads) {
+    const int npad = 8 * gl.ns8 - J;
+#ifdef PSWE_DIAG_NOGTPAD
+    return;
+#endif
+    if (npad <= 0) return;
+    const int per_m = npad * ncol;
+    for (int it = threadIdx.x; it < (R + 1) * per_m; it += nthreads) {
+        const int k = it / per_m, rem = it - k * per_m;
+        const int pr = J + rem / ncol, c = gcol + rem % ncol;
+        const long row = ((((long)z * (R + 1) + k) * gl.ns8 + (pr >> 3)) * 2 + h) * 8 + (pr & 7);
+        gtile[row * gl.sgc + (c ^ gt_swz(gl.ntc, pr & 7))] = 0.0;
+    }
+}
+
 // GT: write the products as forward-Legendre G tiles (GtLayout, pswe_internal.h) instead of
 // Fourier rows [q][m][i]: for each m the block's 5 fields are one 80-byte run.
 template <int N, bool GT>
@@ -335,6 +355,13 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
 #pragma unroll
             for (int q = 0; q < 5; ++q) out[q * rowsz + (long)k * nlat] = make_double2(v[2 * q], v[2 * q + 1]);
         }
+    }
+    if constexpr (GT) {
+        const int J = (nlat + 1) / 2;
+        const bool north = i >= nlat - J;
+        if ((north ? i - (nlat - J) : J - 1 - i) == J - 1)
+            gt_zero_pad(reinterpret_cast<double*>(four_out), gl, R, J, b / gl.spg, north ? 0 : 1,
+                        10 * (b % gl.spg), 10, kIpThreads);
     }
 }
 

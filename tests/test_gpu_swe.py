@@ -212,3 +212,34 @@ def test_empty_batches(P):
     assert g.shape[0] == 0
     assert plan.analyse(g).shape[0] == 0
     torch.cuda.synchronize()
+
+
+def test_tile_padding_not_poisoned(P):
+    """The forward G tiles are one buffer per plan, laid out per batch size: a
+    NaN state evaluated in one layout must not leak into later evaluations / analyses in another
+    through the padding latitude rows (T63 on 96 x 192: 48 latitude pairs, 16 padding rows per
+    32-latitude slice set)."""
+    from paper_1904_05988_b200.cases import balanced_random_state
+    R = 63
+    plan = P.TransformPlan(R, 96, 192)
+    ref = O.TransformPlan(R, 96, 192)
+    p = P.ModelParams(phi_bar=9.80616 * 1e4)
+    po = O.ModelParams(phi_bar=p.phi_bar)
+    good = np.stack([balanced_random_state(R, 20.0, 900 + s, phi_bar=p.phi_bar) for s in range(5)])
+    bad = good.copy()
+    bad[:, 1, 5] = np.nan
+    P.imex_split(cuda(bad), p, plan)  # 5-state layout, NaN everywhere downstream
+    P.imex_split(cuda(bad[:2]), p, plan)  # 2-state layout
+    fe1 = host(P.eval_nonlinear(cuda(good[3]), p, plan))
+    assert np.isfinite(fe1).all()
+    assert rel_diff_fields(fe1, O.eval_nonlinear(good[3], po, ref)) < 1e-11
+    x = fx.micro_bench_fields(R, 7, 3)
+    g = ref.synthesise(x[0])
+    gb = np.stack([ref.synthesise(f) for f in x])
+    P.imex_split(cuda(bad), p, plan)
+    back = host(plan.analyse(cuda(gb)))
+    assert np.isfinite(back).all()
+    assert np.abs(back[0] - ref.analyse(g)).max() < 1e-12 * np.abs(x[0]).max()
+    fe5 = host(P.imex_split(cuda(good), p, plan)[1])
+    for i in range(5):
+        assert rel_diff_fields(fe5[i], O.eval_nonlinear(good[i], po, ref)) < 1e-11
