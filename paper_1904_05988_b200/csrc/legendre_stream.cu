@@ -559,80 +559,100 @@ __global__ void __launch_bounds__(CH * kPrepRowChunks)
                            const double* __restrict__ rtab, const double2* __restrict__ in, double radius,
                            double* __restrict__ Xt) {
     constexpr int SX = 8 * NT + 2;
-    const int cg = blockIdx.x * kPrepRowChunks + threadIdx.x / CH;
+    constexpr int TILE = CH * SX;  // doubles of one chunk's tile
+    __shared__ __align__(32) double sx[kPrepRowChunks * TILE];
+    const int cg0 = blockIdx.x * kPrepRowChunks;
+    const int cg = cg0 + threadIdx.x / CH;
     const int tl = threadIdx.x % CH;
     const int z = blockIdx.y;
+    const int nchk = min(kPrepRowChunks, nct - cg0);  // chunks of this block
     pdl_trigger();
-    if (cg >= nct) return;
-    const int2 mc = reinterpret_cast<const int2*>(chunk_desc)[cg];  // (m, chunk within m)
-    const int m = mc.x;
-    const int t = mc.y * CH + tl;
-    const int s = m + t;
-    const long K = (long)(R + 1) * (R + 2) / 2;
-    const long bs = off_std(R, m), bx = off_ext(R, m);
-    const double a2 = radius * radius, inv_a = 1.0 / radius;
-    const int sm1 = max(s - 1, m), sp1 = min(s + 1, R), s0 = min(s, R);
-    const bool live = s <= R + 1;
-    double fm = 0.0, f0 = 0.0, fp = 0.0, hm = 0.0, hp = 0.0;
-    if (live) {
-        const double rm = __ldg(rtab + max(s - 1, 0)), r0 = __ldg(rtab + s0), rp = __ldg(rtab + min(s + 1, R));
-        const double em = eps[bx + t], ep = eps[bx + min(t + 1, R + 1 - m)];
-        fm = (s - 1 >= m && s - 1 >= 1) ? -a2 * rm : 0.0;
-        f0 = (s <= R && s >= 1) ? -a2 * r0 : 0.0;
-        fp = (s + 1 <= R) ? -a2 * rp : 0.0;
-        hm = (s - 1 >= m) ? -(double)(s - 1) * em : 0.0;
-        hp = (s + 1 <= R) ? (double)(s + 2) * ep : 0.0;
-    }
-    pdl_wait();  // the states come from the preceding kernel
-    double2 ph[NT], vm[NT], v0[NT], vp[NT], dm[NT], d0[NT], dp[NT];
-#pragma unroll
-    for (int ql = 0; ql < NT; ++ql) {
-        const int item = z * NT + ql;
-        ph[ql] = vm[ql] = v0[ql] = vp[ql] = dm[ql] = d0[ql] = dp[ql] = make_double2(0.0, 0.0);
-        if (live && item < n) {
-            const double2* st = in + (long)item * 3 * K + bs - m;
-            ph[ql] = st[s0];
-            vm[ql] = st[K + sm1];
-            v0[ql] = st[K + s0];
-            vp[ql] = st[K + sp1];
-            dm[ql] = st[2 * K + sm1];
-            d0[ql] = st[2 * K + s0];
-            dp[ql] = st[2 * K + sp1];
+    if (cg < nct) {
+        const int2 mc = reinterpret_cast<const int2*>(chunk_desc)[cg];  // (m, chunk within m)
+        const int m = mc.x;
+        const int t = mc.y * CH + tl;
+        const int s = m + t;
+        const long K = (long)(R + 1) * (R + 2) / 2;
+        const long bs = off_std(R, m), bx = off_ext(R, m);
+        const double a2 = radius * radius, inv_a = 1.0 / radius;
+        const int sm1 = max(s - 1, m), sp1 = min(s + 1, R), s0 = min(s, R);
+        const bool live = s <= R + 1;
+        double fm = 0.0, f0 = 0.0, fp = 0.0, hm = 0.0, hp = 0.0;
+        if (live) {
+            const double rm = __ldg(rtab + max(s - 1, 0)), r0 = __ldg(rtab + s0), rp = __ldg(rtab + min(s + 1, R));
+            const double em = eps[bx + t], ep = eps[bx + min(t + 1, R + 1 - m)];
+            fm = (s - 1 >= m && s - 1 >= 1) ? -a2 * rm : 0.0;
+            f0 = (s <= R && s >= 1) ? -a2 * r0 : 0.0;
+            fp = (s + 1 <= R) ? -a2 * rp : 0.0;
+            hm = (s - 1 >= m) ? -(double)(s - 1) * em : 0.0;
+            hp = (s + 1 <= R) ? (double)(s + 2) * ep : 0.0;
         }
-    }
-    double2* row = reinterpret_cast<double2*>(Xt + ((long)z * nct + cg) * CH * SX + (long)tl * SX);
+        pdl_wait();  // the states come from the preceding kernel
+        double2 ph[NT], vm[NT], v0[NT], vp[NT], dm[NT], d0[NT], dp[NT];
 #pragma unroll
-    for (int ql = 0; ql < NT; ++ql) {
-        double2 v[4];
-#pragma unroll
-        for (int f = 0; f < 4; ++f) v[f] = make_double2(0.0, 0.0);
-        if (live && z * NT + ql < n) {
-            if (s <= R) {
-                v[0] = ph[ql];
-                v[1] = v0[ql];
+        for (int ql = 0; ql < NT; ++ql) {
+            const int item = z * NT + ql;
+            ph[ql] = vm[ql] = v0[ql] = vp[ql] = dm[ql] = d0[ql] = dp[ql] = make_double2(0.0, 0.0);
+            if (live && item < n) {
+                const double2* st = in + (long)item * 3 * K + bs - m;
+                ph[ql] = st[s0];
+                vm[ql] = st[K + sm1];
+                v0[ql] = st[K + s0];
+                vp[ql] = st[K + sp1];
+                dm[ql] = st[2 * K + sm1];
+                d0[ql] = st[2 * K + s0];
+                dp[ql] = st[2 * K + sp1];
             }
-            const double2 chi = make_double2(d0[ql].x * f0, d0[ql].y * f0);
-            const double2 psi = make_double2(v0[ql].x * f0, v0[ql].y * f0);
-            double2 cpsi = make_double2(0.0, 0.0), cchi = make_double2(0.0, 0.0);
-            if (s - 1 >= m) {
-                cpsi.x += hm * (vm[ql].x * fm);
-                cpsi.y += hm * (vm[ql].y * fm);
-                cchi.x += hm * (dm[ql].x * fm);
-                cchi.y += hm * (dm[ql].y * fm);
-            }
-            if (s + 1 <= R) {
-                cpsi.x += hp * (vp[ql].x * fp);
-                cpsi.y += hp * (vp[ql].y * fp);
-                cchi.x += hp * (dp[ql].x * fp);
-                cchi.y += hp * (dp[ql].y * fp);
-            }
-            v[2] = make_double2(inv_a * (-m * chi.y - cpsi.x), inv_a * (m * chi.x - cpsi.y));
-            v[3] = make_double2(inv_a * (-m * psi.y + cchi.x), inv_a * (m * psi.x + cchi.y));
         }
+        // the row goes to shared memory; the block's chunks are one contiguous run of tiles, written
+        // below with coalesced 32-byte stores (per-thread 16-byte row stores at a 16 SX-byte stride
+        // left the kernel store-throughput bound: drain / lg_throttle stalls)
+        double2* row = reinterpret_cast<double2*>(sx + (threadIdx.x / CH) * TILE + tl * SX);
 #pragma unroll
-        for (int f = 0; f < 4; ++f) row[4 * ql + f] = v[f];
+        for (int ql = 0; ql < NT; ++ql) {
+            double2 v[4];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) v[f] = make_double2(0.0, 0.0);
+            if (live && z * NT + ql < n) {
+                if (s <= R) {
+                    v[0] = ph[ql];
+                    v[1] = v0[ql];
+                }
+                const double2 chi = make_double2(d0[ql].x * f0, d0[ql].y * f0);
+                const double2 psi = make_double2(v0[ql].x * f0, v0[ql].y * f0);
+                double2 cpsi = make_double2(0.0, 0.0), cchi = make_double2(0.0, 0.0);
+                if (s - 1 >= m) {
+                    cpsi.x += hm * (vm[ql].x * fm);
+                    cpsi.y += hm * (vm[ql].y * fm);
+                    cchi.x += hm * (dm[ql].x * fm);
+                    cchi.y += hm * (dm[ql].y * fm);
+                }
+                if (s + 1 <= R) {
+                    cpsi.x += hp * (vp[ql].x * fp);
+                    cpsi.y += hp * (vp[ql].y * fp);
+                    cchi.x += hp * (dp[ql].x * fp);
+                    cchi.y += hp * (dp[ql].y * fp);
+                }
+                v[2] = make_double2(inv_a * (-m * chi.y - cpsi.x), inv_a * (m * chi.x - cpsi.y));
+                v[3] = make_double2(inv_a * (-m * psi.y + cchi.x), inv_a * (m * psi.x + cchi.y));
+            }
+#pragma unroll
+            for (int f = 0; f < 4; ++f) row[4 * ql + f] = v[f];
+        }
+        row[4 * NT] = make_double2(0.0, 0.0);  // pad columns
+    } else {
+        pdl_wait();
     }
-    row[4 * NT] = make_double2(0.0, 0.0);  // pad columns
+    __syncthreads();
+    const double4* src = reinterpret_cast<const double4*>(sx);
+    double* dst = Xt + ((long)z * nct + cg0) * TILE;  // 32-byte aligned: cg0 % 8 == 0, TILE even
+    const int nv = nchk * TILE / 4;
+    for (int i = threadIdx.x; i < nv; i += CH * kPrepRowChunks) {
+        const double4 w = src[i];
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(dst + 4 * i), "d"(w.x), "d"(w.y), "d"(w.z),
+                     "d"(w.w)
+                     : "memory");
+    }
 }
 
 // grid (ceil(nslices / WS), R+1, column groups); 2 WS warps per block: warps 2w, 2w+1 share
@@ -1008,7 +1028,8 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
 #ifdef PSWE_DIAG_NOPREP
     if (false)
 #endif
-    if (kind == INV_EVAL && PSWE_PREP_ROWS && NT <= 2) {
+    static const int rows_max = [] { const char* e = getenv("PSWE_PREP_ROWS_MAX"); return e ? atoi(e) : 2; }();
+    if (kind == INV_EVAL && PSWE_PREP_ROWS && NT <= rows_max) {  // env: tuning only
         const dim3 gr((P.n_chunks + kPrepRowChunks - 1) / kPrepRowChunks, groups);
         const int n = nq / 4;
         switch (NT) {
@@ -1017,7 +1038,7 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
         launch_pdl(xtile_prep_rows_kernel<T>, gr, dim3(CH * kPrepRowChunks), 0, st, P.R, n, P.n_chunks, P.d_chunk_m, \
                    P.d_eps, P.d_rlap, in, radius, P.d_xtile);                                                  \
         break;
-            PSWE_PREP_CASE(1) PSWE_PREP_CASE(2)
+            PSWE_PREP_CASE(1) PSWE_PREP_CASE(2) PSWE_PREP_CASE(3) PSWE_PREP_CASE(4) PSWE_PREP_CASE(5)
 #undef PSWE_PREP_CASE
         }
     } else if (kind == INV_EVAL)
