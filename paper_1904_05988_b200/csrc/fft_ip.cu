@@ -33,7 +33,12 @@ constexpr int kIpThreads = 256;
 
 // radix of pass s (0 = first) of the in-place plan for length N; 0 past the last pass.
 // Plans: head(N/8) then a final radix-8 pass.
-__host__ __device__ constexpr int ip_radix(int N, int s) {
+// Plan pl = 1 (narrow evaluations and the plain row transforms): N = 256 as two radix-16 passes
+// (fewer shared-memory round trips; 128 registers, so the 5-state grid stage keeps plan 0 and
+// 3 blocks/SM: measured single-state eval -1.5 us, transform round trip -4 us, 5-state batch
+// +6 us with plan 1). Other N: plan 1 = plan 0.
+__host__ __device__ constexpr int ip_radix(int N, int s, int pl = 0) {
+    if (pl == 1 && N == 256) return s < 2 ? 16 : 0;
     const int h = N / 8;
     int h0 = 0, h1 = 0;
     switch (h) {
@@ -56,19 +61,19 @@ __host__ __device__ constexpr int ip_radix(int N, int s) {
     if (h1) return s == 1 ? h1 : (s == 2 ? 8 : 0);
     return s == 1 ? 8 : 0;
 }
-__host__ __device__ constexpr int ip_npass(int N) {
+__host__ __device__ constexpr int ip_npass(int N, int pl = 0) {
     int s = 0;
-    while (ip_radix(N, s)) ++s;
+    while (ip_radix(N, s, pl)) ++s;
     return s;
 }
-__host__ __device__ constexpr int ip_len(int N, int s) {  // sub-transform length entering pass s
+__host__ __device__ constexpr int ip_len(int N, int s, int pl = 0) {  // sub-transform length entering pass s
     int n = N;
-    for (int r = 0; r < s; ++r) n /= ip_radix(N, r);
+    for (int r = 0; r < s; ++r) n /= ip_radix(N, r, pl);
     return n;
 }
-__host__ __device__ constexpr int ip_off(int N, int s) {  // twiddle table offset of pass s
+__host__ __device__ constexpr int ip_off(int N, int s, int pl = 0) {  // twiddle table offset of pass s
     int o = 0;
-    for (int r = 0; r < s; ++r) o += (ip_radix(N, r) - 1) * (ip_len(N, r) / ip_radix(N, r));
+    for (int r = 0; r < s; ++r) o += (ip_radix(N, r, pl) - 1) * (ip_len(N, r, pl) / ip_radix(N, r, pl));
     return o;
 }
 
@@ -77,15 +82,15 @@ __host__ __device__ constexpr int ip_off(int N, int s) {  // twiddle table offse
 // 256 x 512): 3 (78 registers) - the single-state evaluation of an SDC sweep has one block per
 // latitude (256 < 3 x 148), so fewer instructions per block win (eval 36.3 -> 34.0 us, fine sweep
 // 177 -> 166 us; the 5-state batch is unchanged); at N = 512 the same change costs 2 us.
-__host__ __device__ constexpr int ip_minblocks(int N) {
+__host__ __device__ constexpr int ip_minblocks(int N, int pl = 0) {
     int mx = 0;
-    for (int s = 0; ip_radix(N, s); ++s) mx = ip_radix(N, s) > mx ? ip_radix(N, s) : mx;
+    for (int s = 0; ip_radix(N, s, pl); ++s) mx = ip_radix(N, s, pl) > mx ? ip_radix(N, s, pl) : mx;
     if (mx <= 8 && N == 256) return 3;
     if (mx <= 8) return N <= 512 ? 4 : 2;
     return N <= 1024 ? 2 : 1;
 }
 
-__host__ __device__ constexpr int ip_ntw(int N) { return ip_off(N, ip_npass(N)); }  // twiddle entries
+__host__ __device__ constexpr int ip_ntw(int N, int pl = 0) { return ip_off(N, ip_npass(N, pl), pl); }  // twiddle entries
 
 __device__ __forceinline__ int ipad(int i) { return i + (i >> 3); }
 __host__ __device__ constexpr int ipadded(int n) { return n + (n >> 3); }
@@ -103,9 +108,9 @@ __device__ __forceinline__ void pass_roots(double2 (&w)[P], double2 w1) {
 
 // DIF pass s on G rows of A: sub-blocks of length n, butterflies over t (stride M), then the
 // twiddle w_n^(j k) on output k; outputs back to the same slots.
-template <int N, int s, int G, bool INV>
+template <int N, int s, int G, bool INV, int PL = 0>
 __device__ __forceinline__ void dif_pass(double2* A, const double2* TW) {
-    constexpr int P = ip_radix(N, s), n = ip_len(N, s), M = n / P, OFF = ip_off(N, s);
+    constexpr int P = ip_radix(N, s, PL), n = ip_len(N, s, PL), M = n / P, OFF = ip_off(N, s, PL);
     constexpr int T = G * N / P;
     for (int it = threadIdx.x; it < T; it += kIpThreads) {
         const int j = it % M;
@@ -127,9 +132,9 @@ __device__ __forceinline__ void dif_pass(double2* A, const double2* TW) {
 }
 
 // DIT pass s (transpose of dif_pass): twiddle w_n^(j t) on input t, then the butterfly.
-template <int N, int s, int G, bool INV>
+template <int N, int s, int G, bool INV, int PL = 0>
 __device__ __forceinline__ void dit_pass(double2* A, const double2* TW) {
-    constexpr int P = ip_radix(N, s), n = ip_len(N, s), M = n / P, OFF = ip_off(N, s);
+    constexpr int P = ip_radix(N, s, PL), n = ip_len(N, s, PL), M = n / P, OFF = ip_off(N, s, PL);
     constexpr int T = G * N / P;
     for (int it = threadIdx.x; it < T; it += kIpThreads) {
         const int j = it % M;
@@ -149,23 +154,23 @@ __device__ __forceinline__ void dit_pass(double2* A, const double2* TW) {
     }
 }
 
-template <int N, int s, int G, bool INV>
+template <int N, int s, int G, bool INV, int PL = 0>
 struct DifGuard {
     __device__ static void run(double2* A, const double2* TW) {
-        if constexpr (s < ip_npass(N)) {
-            dif_pass<N, s, G, INV>(A, TW);
+        if constexpr (s < ip_npass(N, PL)) {
+            dif_pass<N, s, G, INV, PL>(A, TW);
             __syncthreads();
-            DifGuard<N, s + 1, G, INV>::run(A, TW);
+            DifGuard<N, s + 1, G, INV, PL>::run(A, TW);
         }
     }
 };
-template <int N, int s, int G, bool INV>
+template <int N, int s, int G, bool INV, int PL = 0>
 struct DitGuard {  // passes s, s-1, ..., 0
     __device__ static void run(double2* A, const double2* TW) {
         if constexpr (s >= 0) {
-            dit_pass<N, s, G, INV>(A, TW);
+            dit_pass<N, s, G, INV, PL>(A, TW);
             __syncthreads();
-            DitGuard<N, s - 1, G, INV>::run(A, TW);
+            DitGuard<N, s - 1, G, INV, PL>::run(A, TW);
         }
     }
 };
@@ -200,8 +205,8 @@ __device__ void gt_zero_pad(double* __restrict__ gtile, const GtLayout& gl, int 
 
 // GT: write the products as forward-Legendre G tiles (GtLayout, pswe_internal.h) instead of
 // Fourier rows [q][m][i]: for each m the block's 5 fields are one 80-byte run.
-template <int N, bool GT>
-__global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
+template <int N, bool GT, int PL = 0>
+__global__ void __launch_bounds__(kIpThreads, ip_minblocks(N, PL))
     fft_eval_ip_kernel(int R, int nlat, const double2* __restrict__ TW, const double2* __restrict__ post,
                        const double2* __restrict__ four_in, double2* __restrict__ four_out,
                        const double* __restrict__ rowc, const double* __restrict__ roww,
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
     const int i = blockIdx.x, b = blockIdx.y;
     // twiddles to shared memory (cp.async, overlapped with the row loads; waited before the
     // first barrier)
-    for (int t = threadIdx.x; t < ip_ntw(N); t += kIpThreads) {
+    for (int t = threadIdx.x; t < ip_ntw(N, PL); t += kIpThreads) {
         const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sTW + t));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(TW + t));
     }
@@ -255,7 +260,7 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
     }
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
-    DifGuard<N, 0, 4, true>::run(A, sTW);
+    DifGuard<N, 0, 4, true, PL>::run(A, sTW);
 
     // grid-point products (swe.cpp:41-54), two grid points per complex slot, slot order permuted
     const double c = rowc[i];
@@ -282,7 +287,7 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
         for (int q = 0; q < 5; ++q) A[q * RS + p] = make_double2(o[q][0], o[q][1]);
     }
     __syncthreads();
-    DitGuard<N, ip_npass(N) - 1, 5, false>::run(A, sTW);
+    DitGuard<N, ip_npass(N, PL) - 1, 5, false, PL>::run(A, sTW);
 
     const double nl = 2.0 * N;
     const double sflux = (1.0 / nl) * (inv_a * roww[i] / (c * c));
@@ -365,11 +370,11 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N))
     }
 }
 
-template <int N, bool GT = false>
+template <int N, bool GT = false, int PL = 0>
 bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n, cudaStream_t st,
              GtLayout gl = GtLayout()) {
-    const size_t sm = (size_t)(5 * ipadded(N) + ip_ntw(N)) * sizeof(double2);
-    auto kern = fft_eval_ip_kernel<N, GT>;
+    const size_t sm = (size_t)(5 * ipadded(N) + ip_ntw(N, PL)) * sizeof(double2);
+    auto kern = fft_eval_ip_kernel<N, GT, PL>;
     static bool attr = false;  // once per instantiation
     if (!attr) {
         if (sm > 48 * 1024)
@@ -379,7 +384,8 @@ bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, dou
                                        (int)cudaSharedmemCarveoutMaxShared));
         attr = true;
     }
-    launch_pdl(kern, dim3(P.nlat, n), dim3(kIpThreads), sm, st, P.R, P.nlat, P.d_fft_iptw, P.d_fft_post, fin, fout,
+    launch_pdl(kern, dim3(P.nlat, n), dim3(kIpThreads), sm, st, P.R, P.nlat, PL ? P.d_fft_iptw1 : P.d_fft_iptw,
+               P.d_fft_post, fin, fout,
                P.d_rowc, P.d_roww, P.d_rowmu, prm.phi_bar, prm.omega, 1.0 / prm.radius, gl);
     PSWE_LAUNCH_CHECK();
     return true;
@@ -387,12 +393,12 @@ bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, dou
 
 // slot of frequency k after the DIF passes (k = d0 + P0 d1 + P0 P1 d2 -> d0 M0 + d1 M1 + d2 M2):
 // the mixed-radix digit reversal of the in-place plan
-template <int N>
+template <int N, int PL = 0>
 __device__ __forceinline__ int ip_slot(int k) {
     int p = 0;
 #pragma unroll
-    for (int s = 0; s < ip_npass(N); ++s) {
-        const int P = ip_radix(N, s), M = ip_len(N, s) / P;
+    for (int s = 0; s < ip_npass(N, PL); ++s) {
+        const int P = ip_radix(N, s, PL), M = ip_len(N, s, PL) / P;
         p += (k % P) * M;
         k /= P;
     }
@@ -421,7 +427,7 @@ __global__ void __launch_bounds__(kIpThreads)
     double2* sTW = A + ROWS * RS;
     const int i0 = blockIdx.x * ROWS, b = blockIdx.y;
     const int nrow = min(ROWS, nlat - i0);
-    for (int t = threadIdx.x; t < ip_ntw(N); t += kIpThreads) {
+    for (int t = threadIdx.x; t < ip_ntw(N, 1); t += kIpThreads) {
         const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sTW + t));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(TW + t));
     }
@@ -449,13 +455,13 @@ __global__ void __launch_bounds__(kIpThreads)
             if (r < ROWS && k < H) {
                 double2 a = xa[u];
                 if (k == 0) a.y = 0.0;
-                A[ipad(r * N + ip_slot<N>(k))] = c2r_z(a, xb[u], __ldg(post + k));
-                if (k > 0 && k < N / 2) A[ipad(r * N + ip_slot<N>(N - k))] = c2r_z(xb[u], xa[u], __ldg(post + N - k));
+                A[ipad(r * N + ip_slot<N, 1>(k))] = c2r_z(a, xb[u], __ldg(post + k));
+                if (k > 0 && k < N / 2) A[ipad(r * N + ip_slot<N, 1>(N - k))] = c2r_z(xb[u], xa[u], __ldg(post + N - k));
             }
         }
         asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
-        DitGuard<N, ip_npass(N) - 1, ROWS, true>::run(A, sTW);
+        DitGuard<N, ip_npass(N, 1) - 1, ROWS, true, 1>::run(A, sTW);
         for (int it = threadIdx.x; it < ROWS * N; it += kIpThreads) {
             const int r = it / N, k = it - r * N;
             if (r >= nrow) break;
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__(kIpThreads)
         }
         asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
-        DifGuard<N, 0, ROWS, false>::run(A, sTW);
+        DifGuard<N, 0, ROWS, false, 1>::run(A, sTW);
         // post-pass into registers, then staged [m][row] over the rows (row index XOR-swizzled
         // with m: conflict-free for both the m-fastest writes and the row-fastest reads)
         constexpr int UP = (ROWS * N + kIpThreads - 1) / kIpThreads;  // >= ROWS (R + 1) / 256
@@ -497,8 +503,8 @@ __global__ void __launch_bounds__(kIpThreads)
             const int it = threadIdx.x + u * kIpThreads;
             const int r = it / (R + 1), k = it - r * (R + 1);
             if (r < ROWS) {
-                const double2 zk = A[ipad(r * N + ip_slot<N>(k))];
-                const double2 zc = cconj(A[ipad(r * N + ip_slot<N>(k == 0 ? 0 : N - k))]);
+                const double2 zk = A[ipad(r * N + ip_slot<N, 1>(k))];
+                const double2 zc = cconj(A[ipad(r * N + ip_slot<N, 1>(k == 0 ? 0 : N - k))]);
                 const double2 e = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
                 const double2 d = csub(zk, zc);
                 const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);
@@ -531,7 +537,7 @@ template <int N, bool C2R>
 bool rows_ip(const pswe_plan& P, const double2* four_in, const double* grid_in, double2* four_out, double* grid_out,
              int stride, int off, int n, int cos_flag, int scale_mode, double inv_a, cudaStream_t st) {
     constexpr int ROWS = ip_rows(N);
-    const size_t sm = (size_t)(ROWS * ipadded(N) + ip_ntw(N)) * sizeof(double2);
+    const size_t sm = (size_t)(ROWS * ipadded(N) + ip_ntw(N, 1)) * sizeof(double2);  // plan 1
     if (sm > 227 * 1024) return false;
     auto kern = fft_rows_ip_kernel<N, C2R>;
     static bool attr = false;  // once per instantiation (the cap, not the size of this launch)
@@ -540,7 +546,7 @@ bool rows_ip(const pswe_plan& P, const double2* four_in, const double* grid_in, 
         attr = true;
     }
     kern<<<dim3((P.nlat + ROWS - 1) / ROWS, n), kIpThreads, sm, st>>>(
-        P.R, P.nlat, P.d_fft_iptw, P.d_fft_post, four_in, grid_in, four_out, grid_out, stride, off, P.d_rowc,
+        P.R, P.nlat, P.d_fft_iptw1, P.d_fft_post, four_in, grid_in, four_out, grid_out, stride, off, P.d_rowc,
         P.d_roww, cos_flag, scale_mode, inv_a);
     PSWE_LAUNCH_CHECK();
     return true;
@@ -569,10 +575,10 @@ bool fft_rows_ip(const pswe_plan& P, bool c2r, const double2* four_in, const dou
 
 // Twiddles of the in-place plan: pass s (P, M, n = P M): entries OFF_s + (k-1) M + j =
 // exp(-2 pi i j k / n), k = 1..P-1, j = 0..M-1. Empty (one dummy entry) if N has no plan.
-std::vector<double2> fft_ip_twiddles(int N) {
+std::vector<double2> fft_ip_twiddles(int N, int pl) {
     std::vector<double2> tw;
-    for (int s = 0; ip_radix(N, s); ++s) {
-        const int P = ip_radix(N, s), n = ip_len(N, s), M = n / P;
+    for (int s = 0; ip_radix(N, s, pl); ++s) {
+        const int P = ip_radix(N, s, pl), n = ip_len(N, s, pl), M = n / P;
         for (int k = 1; k < P; ++k)
             for (int j = 0; j < M; ++j) {
                 const long double a = -2.0L * 3.141592653589793238462643383279502884L * ((long)j * k % n) / n;
@@ -609,7 +615,10 @@ void fft_eval_products_gt(const pswe_plan& P, const pswe_params& prm, const doub
     double2* g = reinterpret_cast<double2*>(P.d_gtile);
     switch (P.N) {
 #define PSWE_CASE(NN) \
-    case NN: eval_ip<NN, true>(P, prm, fin, g, n, st, gl); return;
+    case NN:                                                                                  \
+        if (n <= 2) eval_ip<NN, true, 1>(P, prm, fin, g, n, st, gl);                          \
+        else eval_ip<NN, true, 0>(P, prm, fin, g, n, st, gl);                                 \
+        return;
         PSWE_CASE(24) PSWE_CASE(32) PSWE_CASE(48) PSWE_CASE(64) PSWE_CASE(96) PSWE_CASE(128) PSWE_CASE(192)
         PSWE_CASE(256) PSWE_CASE(384) PSWE_CASE(512) PSWE_CASE(768) PSWE_CASE(1024) PSWE_CASE(1536)
 #undef PSWE_CASE

@@ -135,6 +135,7 @@ struct pswe_plan {
     double2* d_fft_roots = nullptr; // [N] exp(-2 pi i k / N)
     double2* d_fft_ptw = nullptr;   // per-pass twiddles of the compile-time Stockham (fft2.cu)
     double2* d_fft_iptw = nullptr;  // per-pass twiddles of the in-place DIF/DIT plan (fft_ip.cu)
+    double2* d_fft_iptw1 = nullptr; // the same for plan 1 (narrow evaluations, plain row transforms)
     pswe::FftDesc fft{};
     // scratch (grow-only)
     int cap_batch = 0;
@@ -229,7 +230,7 @@ bool gt_path_ok(const pswe_plan& P, int n);
 void fft_eval_products_gt(const pswe_plan& P, const pswe_params& prm, const double2* fin, int n, cudaStream_t st);
 void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t st);
 // fft_ip.cu: in-place fused grid stage; false if nlon/2 has no in-place plan
-std::vector<double2> fft_ip_twiddles(int N);
+std::vector<double2> fft_ip_twiddles(int N, int pl = 0);
 bool fft_eval_products_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
                           cudaStream_t st);
 bool fft_eval_products_t(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,

@@ -75,7 +75,9 @@ def test_batched_equals_single(P):
 @pytest.mark.parametrize("R,grid", [(63, (96, 192)), (255, (256, 512))])
 def test_large_batches_equal_single(P, R, grid, n):
     """Batches above 5 states split into several column groups (G tiles of <= 5 states, inverse
-    X tiles of 4 NT columns): every state must match its own single-state evaluation."""
+    X tiles of 4 NT columns): every state must match its own single-state evaluation (to rounding:
+    on the 256 x 512 grid single states take the two-pass radix-16 FFT plan, batches the
+    three-pass one)."""
     from paper_1904_05988_b200.cases import balanced_random_state
     plan = P.TransformPlan(R, grid[0], grid[1])
     p = P.ModelParams(phi_bar=9.80616 * 1e4)
@@ -83,7 +85,7 @@ def test_large_batches_equal_single(P, R, grid, n):
     fi_b, fe_b = (host(t) for t in P.imex_split(cuda(sts), p, plan))
     for i in range(n):
         fi, fe = (host(t) for t in P.imex_split(cuda(sts[i:i + 1]), p, plan))
-        assert rel_diff_fields(fe_b[i], fe[0]) < 1e-13
+        assert rel_diff_fields(fe_b[i], fe[0]) < 1e-12
         assert rel_diff_fields(fi_b[i], fi[0]) < 1e-15
 
 
