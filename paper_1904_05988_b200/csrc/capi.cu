@@ -28,9 +28,12 @@ namespace pswe {
 // (5 projections) -> tail (tendency assembly + linear operator).
 // the evaluation up to the five projections in P.d_proj ([5n][Kx]); the tail (eval_tail, or the
 // SDC sweep's fused tail + node update) turns them into F_E / F_I
-void eval_imex_proj(pswe_plan& P, const pswe_params& prm, const double2* state, int n, cudaStream_t st) {
+// xprep: the state's X tiles were written by the preceding kernel (the SDC sweep's node update,
+// n = 1, xtiles_by_sweep_ok) - the prep launch is skipped
+void eval_imex_proj(pswe_plan& P, const pswe_params& prm, const double2* state, int n, cudaStream_t st, bool xprep) {
     P.reserve(n);
-    legendre_inverse(P, INV_EVAL, state, nullptr, n, prm.radius, P.d_four_a, st);
+    if (xprep) legendre_inverse_prepared(P, P.d_four_a, st);
+    else legendre_inverse(P, INV_EVAL, state, nullptr, n, prm.radius, P.d_four_a, st);
     if (gt_path_ok(P, n)) {  // grid stage writes forward G tiles directly
         fft_eval_products_gt(P, prm, P.d_four_a, n, st);
         legendre_forward_gt(P, n, P.d_proj, st);

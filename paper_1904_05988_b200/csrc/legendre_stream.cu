@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "legendre_common.cuh"
+#include "xrow.cuh"
 
 namespace pswe {
 
@@ -574,19 +575,10 @@ __global__ void __launch_bounds__(CH * kPrepRowChunks)
         const int s = m + t;
         const long K = (long)(R + 1) * (R + 2) / 2;
         const long bs = off_std(R, m), bx = off_ext(R, m);
-        const double a2 = radius * radius, inv_a = 1.0 / radius;
         const int sm1 = max(s - 1, m), sp1 = min(s + 1, R), s0 = min(s, R);
         const bool live = s <= R + 1;
-        double fm = 0.0, f0 = 0.0, fp = 0.0, hm = 0.0, hp = 0.0;
-        if (live) {
-            const double rm = __ldg(rtab + max(s - 1, 0)), r0 = __ldg(rtab + s0), rp = __ldg(rtab + min(s + 1, R));
-            const double em = eps[bx + t], ep = eps[bx + min(t + 1, R + 1 - m)];
-            fm = (s - 1 >= m && s - 1 >= 1) ? -a2 * rm : 0.0;
-            f0 = (s <= R && s >= 1) ? -a2 * r0 : 0.0;
-            fp = (s + 1 <= R) ? -a2 * rp : 0.0;
-            hm = (s - 1 >= m) ? -(double)(s - 1) * em : 0.0;
-            hp = (s + 1 <= R) ? (double)(s + 2) * ep : 0.0;
-        }
+        xrow::Fac F{};
+        if (live) F = xrow::factors(R, m, s, bx, eps, rtab, radius);
         pdl_wait();  // the states come from the preceding kernel
         double2 ph[NT], vm[NT], v0[NT], vp[NT], dm[NT], d0[NT], dp[NT];
 #pragma unroll
@@ -611,30 +603,11 @@ __global__ void __launch_bounds__(CH * kPrepRowChunks)
 #pragma unroll
         for (int ql = 0; ql < NT; ++ql) {
             double2 v[4];
-#pragma unroll
-            for (int f = 0; f < 4; ++f) v[f] = make_double2(0.0, 0.0);
             if (live && z * NT + ql < n) {
-                if (s <= R) {
-                    v[0] = ph[ql];
-                    v[1] = v0[ql];
-                }
-                const double2 chi = make_double2(d0[ql].x * f0, d0[ql].y * f0);
-                const double2 psi = make_double2(v0[ql].x * f0, v0[ql].y * f0);
-                double2 cpsi = make_double2(0.0, 0.0), cchi = make_double2(0.0, 0.0);
-                if (s - 1 >= m) {
-                    cpsi.x += hm * (vm[ql].x * fm);
-                    cpsi.y += hm * (vm[ql].y * fm);
-                    cchi.x += hm * (dm[ql].x * fm);
-                    cchi.y += hm * (dm[ql].y * fm);
-                }
-                if (s + 1 <= R) {
-                    cpsi.x += hp * (vp[ql].x * fp);
-                    cpsi.y += hp * (vp[ql].y * fp);
-                    cchi.x += hp * (dp[ql].x * fp);
-                    cchi.y += hp * (dp[ql].y * fp);
-                }
-                v[2] = make_double2(inv_a * (-m * chi.y - cpsi.x), inv_a * (m * chi.x - cpsi.y));
-                v[3] = make_double2(inv_a * (-m * psi.y + cchi.x), inv_a * (m * psi.x + cchi.y));
+                xrow::columns(F, R, m, s, radius, ph[ql], vm[ql], v0[ql], vp[ql], dm[ql], d0[ql], dp[ql], v);
+            } else {
+#pragma unroll
+                for (int f = 0; f < 4; ++f) v[f] = make_double2(0.0, 0.0);
             }
 #pragma unroll
             for (int f = 0; f < 4; ++f) row[4 * ql + f] = v[f];
@@ -1006,10 +979,8 @@ void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, do
     else fwd_launch<1>(P, four, nq, out, ext, st);
 }
 
-// kind/nq/in/in2/radius as legendre_inverse_mma: tiled prep, then the TMA-pipelined contraction.
-void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq,
-                             double radius, double2* out, cudaStream_t st, cudaEvent_t after_prep) {
-    if (nq <= 0) return;
+// X-tile capacity for nq columns of `kind` (grow-only)
+void xtile_reserve(const pswe_plan& P, int nq, int kind) {
     const int NT = inv_choose_nt(P, nq, kind);
     const int NQ = 4 * NT, SX = 8 * NT + 2;
     const int groups = (nq + NQ - 1) / NQ;
@@ -1019,6 +990,26 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
         PSWE_CUDA(cudaMalloc(&P.d_xtile, need * sizeof(double)));
         P.xtile_cap = need;
     }
+}
+
+// One evaluation state whose X tiles (one column tile, [16][10] per chunk) a preceding kernel has
+// already written - the SDC sweep's node update (sdc.cu): true when the single-state inverse takes
+// this path; then legendre_inverse_prepared runs the contraction alone.
+bool xtiles_by_sweep_ok(const pswe_plan& P) {
+    return !P.simt && use_stream_inverse(P, 4) && inv_choose_nt(P, 4, INV_EVAL) == 1;
+}
+void legendre_inverse_prepared(const pswe_plan& P, double2* out, cudaStream_t st) {
+    inv_tma_launch<1>(P, P.d_xtile, 4, out, st);
+}
+
+// kind/nq/in/in2/radius as legendre_inverse_mma: tiled prep, then the TMA-pipelined contraction.
+void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq,
+                             double radius, double2* out, cudaStream_t st, cudaEvent_t after_prep) {
+    if (nq <= 0) return;
+    const int NT = inv_choose_nt(P, nq, kind);
+    const int NQ = 4 * NT, SX = 8 * NT + 2;
+    const int groups = (nq + NQ - 1) / NQ;
+    xtile_reserve(P, nq, kind);
     const int per = kind == INV_EVAL ? 4 : (kind == INV_UV ? 2 : 1);
     const int nitems = (nq + per - 1) / per;
     const int span = std::max(nitems, groups);  // item slots also zero the groups' pad columns

@@ -203,6 +203,12 @@ void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, do
                              cudaStream_t st);
 // streamed (TMA) inverse chosen over the recurrence inverse for nq columns (legendre_mma.cu)
 bool use_stream_inverse(const pswe_plan& P, int nq);
+void xtile_reserve(const pswe_plan& P, int nq, int kind);
+bool xtiles_by_sweep_ok(const pswe_plan& P);
+void legendre_inverse_prepared(const pswe_plan& P, double2* out, cudaStream_t st);
+// capi.cu: an evaluation up to the five projections in P.d_proj
+void eval_imex_proj(pswe_plan& P, const pswe_params& prm, const double2* state, int n, cudaStream_t st,
+                    bool xprep = false);
 // after_prep (optional): recorded between the prep and the contraction kernel (timing)
 void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, const double2* in2, int nq,
                              double radius, double2* out, cudaStream_t st, cudaEvent_t after_prep = nullptr);

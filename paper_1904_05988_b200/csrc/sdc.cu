@@ -16,11 +16,15 @@
 
 #include "pswe_internal.h"
 #include "tail.cuh"
+#include "xrow.cuh"
+
+#ifndef PSWE_SWEEP_PREP
+#define PSWE_SWEEP_PREP 1
+#endif
 
 namespace pswe {
 void eval_imex(pswe_plan& P, const pswe_params& prm, const double2* state, double2* f_imp, double2* f_exp, int n,
                cudaStream_t st);
-void eval_imex_proj(pswe_plan& P, const pswe_params& prm, const double2* state, int n, cudaStream_t st);
 
 // ---- quadrature tables (quadrature.cpp:19-106) ---------------------------------------------
 
@@ -120,6 +124,10 @@ struct SweepNodeArgs {
     const double* eps;
     int m, M, R;
     double inv_a2, phi_bar, nu;
+    double* xt;           // XP: the new state's X tiles (one column tile, [16][10] per chunk)
+    const int* cbase;     //     chunk base per order m
+    const double* rtab;   //     1/(s(s+1))
+    double radius;
 };
 
 namespace {
@@ -143,15 +151,35 @@ __device__ __forceinline__ int degree_of(int R, long k) {
 // TAIL: the same kernel first finishes node m's evaluation (tail.cuh, the five projections of
 // state m in proj) and writes F_new[m], which the node-m+1 update then takes from registers -
 // one launch fewer per node, the same expressions as eval_tail + sweep_node (tail.cuh).
-template <int NN, bool TAIL>
-__global__ void __launch_bounds__(384) sweep_node_kernel(SweepNodeArgs A) {
-    __shared__ double2 rs[3][128];
+// XP: the block also writes the new state's inverse-Legendre X tiles (the next evaluation's
+// prep, xrow.cuh) - block (130, 3) with one halo coefficient on either side, so the degree
+// neighbours s-1, s+1 of every owned coefficient are in shared memory; the evaluation then skips
+// its prep launch (PSWE_SWEEP_PREP).
+template <int NN, bool TAIL, bool XP>
+__global__ void __launch_bounds__(XP ? 390 : 384) sweep_node_kernel(SweepNodeArgs A) {
+    constexpr int BX = XP ? 130 : 128;
+    __shared__ double2 rs[3][BX];
+    __shared__ double2 snew[XP ? 3 : 1][XP ? BX : 1];
     const long K = (long)(A.R + 1) * (A.R + 2) / 2;
-    const long k = (long)blockIdx.x * 128 + threadIdx.x;
+    const long k = (long)blockIdx.x * 128 + threadIdx.x - (XP ? 1 : 0);
+    const bool owned = !XP || (threadIdx.x >= 1 && threadIdx.x <= 128);
+    const bool valid = k >= 0 && k < K;
     const int f = threadIdx.y;
     pdl_trigger();
+    // XP: the plan constants of this coefficient's X-tile row(s) load before the wait
+    int xm = 0, xs = 0, xcb = 0;
+    xrow::Fac xF{}, xF1{};
+    if constexpr (XP) {
+        if (f == 0 && valid && owned) {
+            tailc::decode_rs(A.R, k, xm, xs);
+            const long bx = off_ext(A.R, xm);
+            xcb = A.cbase[xm];
+            xF = xrow::factors(A.R, xm, xs, bx, A.eps, A.rtab, A.radius);
+            if (xs == A.R) xF1 = xrow::factors(A.R, xm, A.R + 1, bx, A.eps, A.rtab, A.radius);
+        }
+    }
     pdl_wait();  // F and states (TAIL: the projections) come from the preceding kernel
-    if (k < K) {
+    if (valid) {
         const long i = f * K + k;
         double2 fe_m = make_double2(0.0, 0.0), fi_m = make_double2(0.0, 0.0);
         if constexpr (TAIL) {
@@ -160,8 +188,10 @@ __global__ void __launch_bounds__(384) sweep_node_kernel(SweepNodeArgs A) {
             const long Kx = (long)(A.R + 1) * (A.R + 4) / 2;
             tailc::tail_field(f, A.eps, A.proj, Kx, off_ext(A.R, mo), mo, s, -s * (s + 1.0) * A.inv_a2,
                               A.st_m, K, k, A.phi_bar, A.nu, true, fe_m, fi_m);
-            A.fe_new[A.m][i] = fe_m;
-            A.fi_new[A.m][i] = fi_m;
+            if (owned) {
+                A.fe_new[A.m][i] = fe_m;
+                A.fi_new[A.m][i] = fi_m;
+            }
         }
         double2 acc = A.theta0[i];
 #pragma unroll
@@ -180,7 +210,7 @@ __global__ void __launch_bounds__(384) sweep_node_kernel(SweepNodeArgs A) {
             const double2 fij = A.fi_old[j][i], fej = A.fe_old[j][i];
             axpy(acc, A.aq[j], fij);
             axpy(acc, A.aq[j], fej);
-            if (j == 0 && A.fi0_dst) {  // node 0 keeps its right-hand sides (sdc.cpp:22-29)
+            if (j == 0 && A.fi0_dst && owned) {  // node 0 keeps its right-hand sides (sdc.cpp:22-29)
                 A.fi0_dst[i] = fij;
                 A.fe0_dst[i] = fej;
             }
@@ -193,20 +223,62 @@ __global__ void __launch_bounds__(384) sweep_node_kernel(SweepNodeArgs A) {
         rs[f][threadIdx.x] = acc;
     }
     __syncthreads();
-    if (f != 0 || k >= K) return;
-    const double2 r0 = rs[0][threadIdx.x], r1 = rs[1][threadIdx.x], r2 = rs[2][threadIdx.x];
-    const int s = degree_of(A.R, k);
-    const double c = A.aii;
-    const double lam = -s * (s + 1.0) * A.inv_a2;
-    const double diff = 1.0 - c * A.nu * lam;
-    const double2 bp = make_double2(r0.x / diff, r0.y / diff);
-    const double2 bz = make_double2(r1.x / diff, r1.y / diff);
-    const double2 bd = make_double2(r2.x / diff, r2.y / diff);
-    const double ce = c / diff;
-    const double det = 1.0 - ce * ce * A.phi_bar * lam;
-    A.out[k] = make_double2((bp.x - ce * A.phi_bar * bd.x) / det, (bp.y - ce * A.phi_bar * bd.y) / det);
-    A.out[2 * K + k] = make_double2((bd.x - ce * lam * bp.x) / det, (bd.y - ce * lam * bp.y) / det);
-    A.out[K + k] = bz;
+    int s = 0;
+    if (f == 0 && valid) {
+        const double2 r0 = rs[0][threadIdx.x], r1 = rs[1][threadIdx.x], r2 = rs[2][threadIdx.x];
+        s = degree_of(A.R, k);
+        const double c = A.aii;
+        const double lam = -s * (s + 1.0) * A.inv_a2;
+        const double diff = 1.0 - c * A.nu * lam;
+        const double2 bp = make_double2(r0.x / diff, r0.y / diff);
+        const double2 bz = make_double2(r1.x / diff, r1.y / diff);
+        const double2 bd = make_double2(r2.x / diff, r2.y / diff);
+        const double ce = c / diff;
+        const double det = 1.0 - ce * ce * A.phi_bar * lam;
+        const double2 nph = make_double2((bp.x - ce * A.phi_bar * bd.x) / det, (bp.y - ce * A.phi_bar * bd.y) / det);
+        const double2 ndv = make_double2((bd.x - ce * lam * bp.x) / det, (bd.y - ce * lam * bp.y) / det);
+        if (owned) {
+            A.out[k] = nph;
+            A.out[2 * K + k] = ndv;
+            A.out[K + k] = bz;
+        }
+        if constexpr (XP) {
+            snew[0][threadIdx.x] = nph;
+            snew[1][threadIdx.x] = bz;
+            snew[2][threadIdx.x] = ndv;
+        }
+    }
+    if constexpr (XP) {
+        __syncthreads();
+        if (f != 0 || !valid || !owned) return;
+        const int m = xm, R = A.R, x = threadIdx.x, cb = xcb;
+        s = xs;
+        // degree s' of this order: shared-memory slot of the clamped neighbour (the halo holds the
+        // coefficients k0 - 1 and k0 + 128; clamped positions are never used by xrow::columns)
+        auto at = [&](int fld, int sp) { return snew[fld][x + (min(max(sp, m), R) - s)]; };
+        auto emit = [&](int sd, const xrow::Fac& F) {  // X-tile row of degree sd (s or R+1)
+            const int t = sd - m;
+            double2 v[4];
+            xrow::columns(F, R, m, sd, A.radius, at(0, sd), at(1, sd - 1), at(1, sd), at(1, sd + 1), at(2, sd - 1),
+                          at(2, sd), at(2, sd + 1), v);
+            double2* row = reinterpret_cast<double2*>(A.xt + ((long)(cb + t / 16) * 16 + (t & 15)) * 10);
+            row[0] = v[0];
+            row[1] = v[1];
+            row[2] = v[2];
+            row[3] = v[3];
+            row[4] = make_double2(0.0, 0.0);
+        };
+        emit(s, xF);
+        if (s == R) {  // the extra degree R+1 (H-sum terms), then zero rows to the end of the chunk
+            emit(R + 1, xF1);
+            const int nrow = (R + 2 - m + 15) / 16 * 16;
+            for (int t = R + 2 - m; t < nrow; ++t) {
+                double2* row = reinterpret_cast<double2*>(A.xt + ((long)(cb + t / 16) * 16 + (t & 15)) * 10);
+#pragma unroll
+                for (int c = 0; c < 5; ++c) row[c] = make_double2(0.0, 0.0);
+            }
+        }
+    }
 }
 
 struct ResidualArgs {
@@ -426,6 +498,12 @@ void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) 
     // the first node's update kernel copies them into the new buffer
     (void)bytes;
     const Tables& t = L->tab;
+    // the node update also writes the next evaluation's X tiles (its prep launch is skipped)
+    static const bool xp_env = [] { const char* e = getenv("PSWE_NO_SWEEP_PREP"); return !(e && atoi(e) != 0); }();
+    // (measured per level size: T255 5-node sweep -5.6%, T255 3-node -5%, T127 even, T511 +4.8% - the
+    // larger update kernel then costs more than the prep launch it saves)
+    const bool xp = PSWE_SWEEP_PREP && xp_env && L->K <= 65536 && xtiles_by_sweep_ok(*L->plan);
+    if (xp) xtile_reserve(*L->plan, 4, INV_EVAL);
     for (int m = 0; m < M; ++m) {
         SweepNodeArgs A{};
         A.theta0 = L->st(0);
@@ -451,25 +529,31 @@ void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) 
         A.inv_a2 = 1.0 / (L->prm.radius * L->prm.radius);
         A.phi_bar = L->prm.phi_bar;
         A.nu = L->prm.nu;
-        const dim3 grid((unsigned)((L->K + 127) / 128)), block(128, 3);
+        const dim3 grid((unsigned)((L->K + 127) / 128)), block(xp ? 130 : 128, 3);
+        A.eps = L->plan->d_eps;
+        if (xp) {
+            A.xt = L->plan->d_xtile;
+            A.cbase = L->plan->d_chk_off;
+            A.rtab = L->plan->d_rlap;
+            A.radius = L->prm.radius;
+        }
         if (m > 0) {  // finish node m's evaluation in the same kernel
             A.proj = L->plan->d_proj;
             A.st_m = L->st(m);
-            A.eps = L->plan->d_eps;
-            switch (L->nn) {
-                case 2: launch_pdl(sweep_node_kernel<2, true>, grid, block, 0, st, A); break;
-                case 3: launch_pdl(sweep_node_kernel<3, true>, grid, block, 0, st, A); break;
-                default: launch_pdl(sweep_node_kernel<5, true>, grid, block, 0, st, A); break;
-            }
-        } else {
-            switch (L->nn) {
-                case 2: launch_pdl(sweep_node_kernel<2, false>, grid, block, 0, st, A); break;
-                case 3: launch_pdl(sweep_node_kernel<3, false>, grid, block, 0, st, A); break;
-                default: launch_pdl(sweep_node_kernel<5, false>, grid, block, 0, st, A); break;
-            }
         }
+#define PSWE_SWEEP_LAUNCH(NN)                                                                   \
+    if (m > 0 && xp) launch_pdl(sweep_node_kernel<NN, true, true>, grid, block, 0, st, A);      \
+    else if (m > 0) launch_pdl(sweep_node_kernel<NN, true, false>, grid, block, 0, st, A);      \
+    else if (xp) launch_pdl(sweep_node_kernel<NN, false, true>, grid, block, 0, st, A);         \
+    else launch_pdl(sweep_node_kernel<NN, false, false>, grid, block, 0, st, A);
+        switch (L->nn) {
+            case 2: PSWE_SWEEP_LAUNCH(2) break;
+            case 3: PSWE_SWEEP_LAUNCH(3) break;
+            default: PSWE_SWEEP_LAUNCH(5) break;
+        }
+#undef PSWE_SWEEP_LAUNCH
         PSWE_LAUNCH_CHECK();
-        eval_imex_proj(*L->plan, L->prm, L->st(m + 1), 1, st);
+        eval_imex_proj(*L->plan, L->prm, L->st(m + 1), 1, st, xp);
     }
     eval_tail(*L->plan, L->prm, L->plan->d_proj, L->st(M), L->fi(M, nw), L->fe(M, nw), 1, st);
     L->cur = nw;

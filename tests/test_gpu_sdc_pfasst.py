@@ -137,3 +137,22 @@ def test_level_rejects_unsupported_node_counts(P):
     for nn in (1, 4, 6):
         with pytest.raises(P._lib.PsweError):
             P.Level(plan, P.ModelParams(), nn)
+
+
+def test_sweep_emitted_xtiles_bit_identical(tmp_path):
+    """The SDC node update writes the next evaluation's X tiles itself (the prep launch skipped);
+    the sweeps must give the same bits as with the separate prep kernel (PSWE_NO_SWEEP_PREP=1),
+    at T255 / 5 nodes, T127 / 3 nodes (fused) and T63 / 2 nodes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ("0", "1"):
+        out = tmp_path / f"sw{env}.npz"
+        subprocess.run([sys.executable, os.path.join(root, "tools", "sweep_dump.py"), str(out)], check=True,
+                       env={**os.environ, "PSWE_NO_SWEEP_PREP": env}, timeout=300)
+        outs.append(np.load(out))
+    assert sorted(outs[0].files) == sorted(outs[1].files)
+    for k in outs[0].files:
+        np.testing.assert_array_equal(outs[0][k], outs[1][k])

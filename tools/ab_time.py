@@ -74,7 +74,7 @@ for R, nlat, nlon in ((255, 256, 512), (511, 512, 1024)):
                                        (round(float(v) * 1e3, 1) for v in np.median(np.array(ks), axis=0))))
     del plan
 # one fine SDC sweep (5 nodes: 4 single-state evaluations + node updates) and one coarse sweep
-for R, nlat, nlon, nn in ((255, 256, 512, 5), (127, 128, 256, 3)):
+for R, nlat, nlon, nn in ((255, 256, 512, 5), (127, 128, 256, 3), (511, 512, 1024, 5), (255, 256, 512, 3)):
     lvl = P.Level(P.TransformPlan(R, nlat, nlon), prm, nn)
     lvl.spread(torch.as_tensor(balanced_random_state(R, 40.0, 3)).cuda())
     for _ in range(5):
