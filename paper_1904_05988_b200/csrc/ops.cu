@@ -22,10 +22,16 @@ __global__ void eval_tail_kernel(int R, const double* __restrict__ eps, const do
     const long k = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const int b = blockIdx.y;
     pdl_trigger();
+    // plan constants first: they overlap the forward kernel's tail
+    int m = 0, s = 0;
+    double eu = 0.0, el = 0.0;
+    if (k < K) {
+        decode_rs(R, k, m, s);
+        eu = eps[off_ext(R, m) + s - m + 1];
+        el = eps[off_ext(R, m) + s - m];
+    }
     pdl_wait();  // the projections come from the forward Legendre kernel
     if (k >= K) return;
-    int m, s;
-    decode_rs(R, k, m, s);
     const long bx = off_ext(R, m);
     const double2* A = proj + (long)b * 5 * Kx;
     const double lam = -s * (s + 1.0) * inv_a2;
@@ -35,7 +41,7 @@ __global__ void eval_tail_kernel(int R, const double* __restrict__ eps, const do
     double2 e[3], i[3];  // every load before any store
 #pragma unroll
     for (int f = 0; f < 3; ++f)
-        tailc::tail_field(f, eps, A, Kx, bx, m, s, lam, st, K, k, phi_bar, nu, fi != nullptr, e[f], i[f]);
+        tailc::tail_field(f, eu, el, A, Kx, bx, m, s, lam, st, K, k, phi_bar, nu, fi != nullptr, e[f], i[f]);
 #pragma unroll
     for (int f = 0; f < 3; ++f) {
         fe[f * K + k] = e[f];

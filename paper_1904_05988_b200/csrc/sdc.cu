@@ -169,6 +169,16 @@ __global__ void __launch_bounds__(XP ? 390 : 384) sweep_node_kernel(SweepNodeArg
     // XP: the plan constants of this coefficient's X-tile row(s) load before the wait
     int xm = 0, xs = 0, xcb = 0;
     xrow::Fac xF{}, xF1{};
+    // TAIL: node m's (order, degree) and its eps pair are plan constants too
+    int tm = 0, ts = 0;
+    double teu = 0.0, tel = 0.0;
+    if constexpr (TAIL) {
+        if (valid) {
+            tailc::decode_rs(A.R, k, tm, ts);
+            teu = A.eps[off_ext(A.R, tm) + ts - tm + 1];
+            tel = A.eps[off_ext(A.R, tm) + ts - tm];
+        }
+    }
     if constexpr (XP) {
         if (f == 0 && valid && owned) {
             tailc::decode_rs(A.R, k, xm, xs);
@@ -183,10 +193,8 @@ __global__ void __launch_bounds__(XP ? 390 : 384) sweep_node_kernel(SweepNodeArg
         const long i = f * K + k;
         double2 fe_m = make_double2(0.0, 0.0), fi_m = make_double2(0.0, 0.0);
         if constexpr (TAIL) {
-            int mo, s;
-            tailc::decode_rs(A.R, k, mo, s);
             const long Kx = (long)(A.R + 1) * (A.R + 4) / 2;
-            tailc::tail_field(f, A.eps, A.proj, Kx, off_ext(A.R, mo), mo, s, -s * (s + 1.0) * A.inv_a2,
+            tailc::tail_field(f, teu, tel, A.proj, Kx, off_ext(A.R, tm), tm, ts, -ts * (ts + 1.0) * A.inv_a2,
                               A.st_m, K, k, A.phi_bar, A.nu, true, fe_m, fi_m);
             if (owned) {
                 A.fe_new[A.m][i] = fe_m;

@@ -21,13 +21,13 @@ __device__ __forceinline__ void decode_rs(int R, long k, int& m, int& s) {
 }
 
 // H-combination of a projection A (extended layout, block m): H_s = -s eps_{s+1} A_{s+1} + (s+1) eps_s A_{s-1}
-// (the lower neighbour's load is clamped rather than branched, so all loads issue together)
-__device__ __forceinline__ double2 hcomb(const double2* __restrict__ A, const double* __restrict__ eps, long bx,
-                                         int m, int s) {
+// (the lower neighbour's load is clamped rather than branched, so all loads issue together);
+// eu = eps_{s+1}, el = eps_s (plan constants: loaded before the programmatic-launch wait)
+__device__ __forceinline__ double2 hcomb(const double2* __restrict__ A, double eu, double el, long bx, int m,
+                                         int s) {
     const int t = s - m;
-    const double fu = -(double)s * eps[bx + t + 1];
+    const double fu = -(double)s * eu;
     const double2 up = A[bx + t + 1];
-    const double el = eps[bx + t];
     const double2 lo = A[bx + (t > 0 ? t - 1 : 0)];
     double2 h = make_double2(fu * up.x, fu * up.y);
     if (t > 0) {
@@ -37,21 +37,25 @@ __device__ __forceinline__ double2 hcomb(const double2* __restrict__ A, const do
     }
     return h;
 }
+__device__ __forceinline__ double2 hcomb(const double2* __restrict__ A, const double* __restrict__ eps, long bx,
+                                         int m, int s) {
+    return hcomb(A, eps[bx + s - m + 1], eps[bx + s - m], bx, m, s);
+}
 
 // Field f (0 Phi, 1 zeta, 2 delta) of the eval_nonlinear assembly (swe.cpp:61-67) from the five
-// projections A1..A5 (A = proj of this state, extended layout, s = m..R+1) and of eval_linear
+// projections A1..A5 (A = proj of this state, extended layout, s = m..R+1; eu, el as hcomb) and of eval_linear
 // (swe.cpp:9-25, only if need_fi) of the state st (3K) at coefficient k = (m, s), lam = -s(s+1)/a^2:
 //   Phi_t  = -(i m A1 - H[A2])          (-flux_div)
 //   zeta_t = -(i m A3 - H[A4])          (-q_div)
 //   div_t  = (i m A4 + H[A3]) - lap(A5) (q_curl - lap ke)
-__device__ __forceinline__ void tail_field(int f, const double* __restrict__ eps, const double2* __restrict__ A,
+__device__ __forceinline__ void tail_field(int f, double eu, double el, const double2* __restrict__ A,
                                            long Kx, long bx, int m, int s, double lam,
                                            const double2* __restrict__ st, long K, long k, double phi_bar,
                                            double nu, bool need_fi, double2& fe, double2& fi) {
     const long o = bx + s - m;
     if (f == 0) {
         const double2 a1 = A[o];
-        const double2 h2 = hcomb(A + Kx, eps, bx, m, s);
+        const double2 h2 = hcomb(A + Kx, eu, el, bx, m, s);
         const double2 fdiv = make_double2(-m * a1.y - h2.x, m * a1.x - h2.y);
         fe = make_double2(-fdiv.x, -fdiv.y);
         if (!need_fi) return;
@@ -59,7 +63,7 @@ __device__ __forceinline__ void tail_field(int f, const double* __restrict__ eps
         fi = make_double2(-phi_bar * dv.x + nu * lam * ph.x, -phi_bar * dv.y + nu * lam * ph.y);
     } else if (f == 1) {
         const double2 a3 = A[2 * Kx + o];
-        const double2 h4 = hcomb(A + 3 * Kx, eps, bx, m, s);
+        const double2 h4 = hcomb(A + 3 * Kx, eu, el, bx, m, s);
         const double2 qdiv = make_double2(-m * a3.y - h4.x, m * a3.x - h4.y);
         fe = make_double2(-qdiv.x, -qdiv.y);
         if (!need_fi) return;
@@ -67,7 +71,7 @@ __device__ __forceinline__ void tail_field(int f, const double* __restrict__ eps
         fi = make_double2(nu * lam * vo.x, nu * lam * vo.y);
     } else {
         const double2 a4 = A[3 * Kx + o], a5 = A[4 * Kx + o];
-        const double2 h3 = hcomb(A + 2 * Kx, eps, bx, m, s);
+        const double2 h3 = hcomb(A + 2 * Kx, eu, el, bx, m, s);
         const double2 qcurl = make_double2(-m * a4.y + h3.x, m * a4.x + h3.y);
         const double2 kel = make_double2(lam * a5.x, lam * a5.y);
         fe = make_double2(qcurl.x - kel.x, qcurl.y - kel.y);
