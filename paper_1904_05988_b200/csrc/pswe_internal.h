@@ -288,6 +288,8 @@ struct pswe_level {
     double2* d_f[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [buffer][0=imp,1=exp] -> [nn][3K]
     int cur = 0;
     unsigned long long* d_res = nullptr;
+    unsigned long long* d_bmax = nullptr;  // residual: per-block maxima
+    unsigned int* d_count = nullptr;       // residual: blocks done (0 between launches)
     double2* st(int node) const { return d_state + (size_t)node * 3 * K; }
     double2* fi(int node, int buf = -1) const { return d_f[buf < 0 ? cur : buf][0] + (size_t)node * 3 * K; }
     double2* fe(int node, int buf = -1) const { return d_f[buf < 0 ? cur : buf][1] + (size_t)node * 3 * K; }

@@ -296,6 +296,8 @@ struct ResidualArgs {
     double w[kMaxNodes][kMaxNodes];  // -dt*q(m,j)
     int nn;
     long n3;  // 3K
+    unsigned long long* bmax;  // per-block maxima (bit patterns of non-negative doubles)
+    unsigned int* count;       // blocks done; the last block reduces and resets it to 0
 };
 
 // F_I, F_E of every node loaded once per coefficient and reused for all NN rows (same axpy order)
@@ -333,8 +335,43 @@ __global__ void residual_kernel(ResidualArgs A, unsigned long long* out) {
     if (threadIdx.x < 32) {
         mx = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0.0;
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(mx));
+        if (threadIdx.x == 0) {
+            A.bmax[blockIdx.x] = (unsigned long long)__double_as_longlong(mx);
+            __threadfence();
+            wm[0] = atomicAdd(A.count, 1u) == gridDim.x - 1 ? 1.0 : 0.0;
+        }
     }
+    // the last block to finish reduces the block maxima (max is order-independent, so the result
+    // is deterministic) - no zeroing of *out beforehand
+    __syncthreads();
+    if (wm[0] == 0.0) return;
+    __threadfence();
+    unsigned long long b = 0ull;
+    for (unsigned j = threadIdx.x; j < gridDim.x; j += blockDim.x) b = max(b, __ldcg(A.bmax + j));
+    for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    __shared__ unsigned long long wb[32];
+    if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b = max(b, wb[w]);
+        *out = b;
+        *A.count = 0u;
+    }
+}
+
+struct CopyArgs {
+    double2* dst[8];
+    const double2* src[8];
+    long len;  // double2 per pair
+};
+// n device-to-device copies in one launch (blockIdx.y = pair): a kernel rather than memcpy nodes,
+// so the stream / graph chain keeps its programmatic-launch overlap
+__global__ void copy_kernel(CopyArgs A) {
+    pdl_trigger();
+    pdl_wait();
+    const int p = blockIdx.y;
+    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < A.len; i += (long)gridDim.x * blockDim.x)
+        A.dst[p][i] = A.src[p][i];
 }
 
 // coarse coefficient kc of a state (3 fields) -> fine coefficient index
@@ -480,20 +517,38 @@ using namespace pswe;
 
 namespace pswe {
 
+static void copies(const std::vector<std::pair<double2*, const double2*>>& cp, long len, cudaStream_t st) {
+    for (size_t b = 0; b < cp.size(); b += 8) {
+        CopyArgs A{};
+        const int n = (int)std::min<size_t>(8, cp.size() - b);
+        for (int i = 0; i < n; ++i) {
+            A.dst[i] = cp[b + i].first;
+            A.src[i] = cp[b + i].second;
+        }
+        A.len = len;
+        const unsigned gx = (unsigned)std::min<long>((len + 255) / 256, 296);
+        launch_pdl(copy_kernel, dim3(gx, n), dim3(256), 0, st, A);
+        PSWE_LAUNCH_CHECK();
+    }
+}
+
 static void refresh(pswe_level* L, int first, int count, cudaStream_t st) {
     if (count <= 0) return;
     eval_imex(*L->plan, L->prm, L->st(first), L->fi(first), L->fe(first), count, st);
 }
 
 void level_spread(pswe_level* L, const double2* theta0, cudaStream_t st) {
-    const size_t bytes = 3 * L->K * sizeof(double2);
+    std::vector<std::pair<double2*, const double2*>> cp;
     for (int m = 0; m < L->nn; ++m)
-        if (L->st(m) != theta0) PSWE_CUDA(cudaMemcpyAsync(L->st(m), theta0, bytes, cudaMemcpyDeviceToDevice, st));
+        if (L->st(m) != theta0) cp.push_back({L->st(m), theta0});
+    copies(cp, 3 * L->K, st);
     refresh(L, 0, 1, st);
+    cp.clear();
     for (int m = 1; m < L->nn; ++m) {
-        PSWE_CUDA(cudaMemcpyAsync(L->fi(m), L->fi(0), bytes, cudaMemcpyDeviceToDevice, st));
-        PSWE_CUDA(cudaMemcpyAsync(L->fe(m), L->fe(0), bytes, cudaMemcpyDeviceToDevice, st));
+        cp.push_back({L->fi(m), L->fi(0)});
+        cp.push_back({L->fe(m), L->fe(0)});
     }
+    copies(cp, 3 * L->K, st);
 }
 
 void level_refresh(pswe_level* L, int first, int count, cudaStream_t st) { refresh(L, first, count, st); }
@@ -577,9 +632,10 @@ void level_residual(pswe_level* L, double dt, double* out, cudaStream_t st) {
         A.fe[m] = L->fe(m);
         for (int j = 0; j < L->nn; ++j) A.w[m][j] = -dt * L->tab.Q(m, j);
     }
-    PSWE_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
     const int bs = 256;
     const unsigned g = (unsigned)((A.n3 + bs - 1) / bs);
+    A.bmax = L->d_bmax;
+    A.count = L->d_count;
     auto* o = reinterpret_cast<unsigned long long*>(out);
     switch (L->nn) {
         case 2: launch_pdl(residual_kernel<2>, dim3(g), dim3(bs), 0, st, A, o); break;
@@ -632,10 +688,8 @@ void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st, const doub
 
 void pair_save(pswe_pair* P, cudaStream_t st) {
     pswe_level* C = P->coarse;
-    const size_t bytes = (size_t)C->nn * 3 * C->K * sizeof(double2);
-    PSWE_CUDA(cudaMemcpyAsync(P->saved(0, 0), C->st(0), bytes, cudaMemcpyDeviceToDevice, st));
-    PSWE_CUDA(cudaMemcpyAsync(P->saved(1, 0), C->fi(0), bytes, cudaMemcpyDeviceToDevice, st));
-    PSWE_CUDA(cudaMemcpyAsync(P->saved(2, 0), C->fe(0), bytes, cudaMemcpyDeviceToDevice, st));
+    copies({{P->saved(0, 0), C->st(0)}, {P->saved(1, 0), C->fi(0)}, {P->saved(2, 0), C->fe(0)}},
+           (long)C->nn * 3 * C->K, st);
 }
 
 void pair_interp_increment_add(pswe_pair* P, double2* dstate0, cudaStream_t st) {
@@ -742,9 +796,15 @@ int pswe_level_create(pswe_plan* plan, const pswe_params* p, int num_nodes, pswe
             for (int b = 0; b < 2; ++b)
                 for (int k = 0; k < 2; ++k) PSWE_CUDA(cudaMalloc(&L->d_f[b][k], bytes));
             PSWE_CUDA(cudaMemset(L->d_state, 0, bytes));
+            const size_t nblk = (size_t)(3 * L->K + 255) / 256;  // residual_kernel's grid
+            PSWE_CUDA(cudaMalloc(&L->d_bmax, nblk * sizeof(unsigned long long)));
+            PSWE_CUDA(cudaMalloc(&L->d_count, sizeof(unsigned int)));
+            PSWE_CUDA(cudaMemset(L->d_count, 0, sizeof(unsigned int)));
             plan->reserve(num_nodes);
         } catch (...) {
             if (L->d_state) cudaFree(L->d_state);
+            if (L->d_bmax) cudaFree(L->d_bmax);
+            if (L->d_count) cudaFree(L->d_count);
             for (auto& b : L->d_f)
                 for (auto* q : b)
                     if (q) cudaFree(q);
@@ -759,6 +819,8 @@ int pswe_level_destroy(pswe_level* L) {
     return guarded([&] {
         if (!L) return;
         cudaFree(L->d_state);
+        if (L->d_bmax) cudaFree(L->d_bmax);
+        if (L->d_count) cudaFree(L->d_count);
         for (auto& b : L->d_f)
             for (auto* q : b) cudaFree(q);
         delete L;
