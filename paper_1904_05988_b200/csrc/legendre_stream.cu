@@ -440,6 +440,146 @@ void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out,
     PSWE_LAUNCH_CHECK();
 }
 
+// ---- forward, narrow column groups: P fragments straight from the table into registers --------
+// PSWE_FWD_DIRECT (default): for one/two-state batches (NTC <= 3) on grids of up to NSL 32-latitude
+// slices, every warp loads ALL the B fragments of its chunk (NSL x 8 k-steps x {even, odd} - one
+// 8-byte value per lane each, 4 rows x 8 columns of a swizzled P tile per warp instruction: full
+// sectors) into registers BEFORE the programmatic-launch wait, so the P table read (the kernel's
+// dominant traffic, plan constants) overlaps the grid stage that precedes it; after the wait only
+// the G tiles of the task's (at most two) orders arrive, as one bulk copy each into shared memory.
+// Same task table, fragment maps, arithmetic order and epilogue as leg_fwd_gt_kernel<NTC, 8, 1>
+// (bit-identical results).
+#ifndef PSWE_FWD_DIRECT
+#define PSWE_FWD_DIRECT 1
+#endif
+template <int NTC, int NSL>
+__global__ void __launch_bounds__(256, 2) leg_fwd_gt_direct_kernel(int R, int Jp, int nq, GtLayout gl,
+                                                                  const double* __restrict__ ptab,
+                                                                  const int* __restrict__ cbase,
+                                                                  const int4* __restrict__ tasks_a,
+                                                                  const int2* __restrict__ tasks_b,
+                                                                  const double* __restrict__ gt,
+                                                                  double2* __restrict__ out) {
+    constexpr int W = 8;
+    extern __shared__ __align__(128) double smem[];
+    const int sgc = gl.sgc;
+    const int gsub = 2 * 8 * sgc;      // doubles of one 8-latitude slice of one order's G
+    const int ns8 = gl.ns8;            // = 4 NSL
+    double* sG = smem;                 // [2 orders][ns8][2][8][sgc]
+    __shared__ unsigned long long full;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int4 ta = tasks_a[blockIdx.x];
+    const int2 tb = tasks_b[blockIdx.x];
+    const int na = ta.z, nb = tb.y;
+    const int z = blockIdx.y;
+    const bool ord_b = warp >= na;
+    const int my_m = ord_b ? ta.w : ta.x;
+    const int my_c = ord_b ? tb.x + (warp - na) : ta.y + warp;
+    const bool mine = ord_b ? warp - na < nb : true;
+    const int r4 = lane >> 2, c4 = lane & 3;
+    if (threadIdx.x == 0) {
+        mbar_init(&full, 1);
+        mbar_fence_init();
+    }
+    // B fragments of this warp's chunk: a two-slice register window (slice sl in pb[sl & 1]), 8-latitude
+    // sub-slice u, k-step ks, parity; slices 0 and 1 load before the wait, slice sl + 2 as soon as
+    // slice sl has been consumed
+    double pb[2][4][2][2];
+    const double* pt = ptab;
+    long pstride = 0;
+    auto load_slice = [&](int sl) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const double* row = pt + sl * pstride + (8 * u + 4 * ks + c4) * 16;
+                pb[sl & 1][u][ks][0] = row[pswz(c4, r4)];
+                pb[sl & 1][u][ks][1] = row[pswz(c4, 8 + r4)];
+            }
+    };
+    if (mine) {
+        const int nchm = (R + 2 - my_m + CH - 1) / CH;
+        pt = ptab + ptile_off(cbase[my_m], nchm, Jp >> 5, my_c, 0);
+        pstride = (long)nchm * 512;
+        load_slice(0);
+        if (NSL > 1) load_slice(1);
+    }
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();  // G tiles come from the grid stage
+    if (threadIdx.x == 0) {
+        const unsigned GB = (unsigned)(ns8 * gsub) * sizeof(double);
+        mbar_expect_tx(&full, GB * (nb > 0 ? 2u : 1u));
+        bulk_g2s(sG, gt + ((long)z * (R + 1) + ta.x) * ns8 * gsub, GB, &full);
+        if (nb > 0) bulk_g2s(sG + ns8 * gsub, gt + ((long)z * (R + 1) + ta.w) * ns8 * gsub, GB, &full);
+    }
+    double acc[NTC][2][2];
+#pragma unroll
+    for (int a = 0; a < NTC; ++a) acc[a][0][0] = acc[a][0][1] = acc[a][1][0] = acc[a][1][1] = 0.0;
+    mbar_wait(&full, 0u);
+    if (!mine) return;
+    const double* gbase = sG + (ord_b ? ns8 * gsub : 0);
+#pragma unroll
+    for (int sl = 0; sl < NSL; ++sl) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double* g = gbase + (4 * sl + u) * gsub;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+                const int rr = 4 * ks + c4;
+                double ae[NTC], ao[NTC];
+#pragma unroll
+                for (int nt = 0; nt < NTC; ++nt) {
+                    const int cs = (8 * nt + r4) ^ gt_swz(NTC, rr);
+                    const double gn = g[rr * sgc + cs];
+                    const double gs = g[(8 + rr) * sgc + cs];
+                    ae[nt] = gn + gs;
+                    ao[nt] = gn - gs;
+                }
+#pragma unroll
+                for (int nt = 0; nt < NTC; ++nt) {
+                    dmma(acc[nt][0], ae[nt], pb[sl & 1][u][ks][0]);
+                    dmma(acc[nt][1], ao[nt], pb[sl & 1][u][ks][1]);
+                }
+            }
+        }
+        if (sl + 2 < NSL) load_slice(sl + 2);
+    }
+    const long Kx = (long)(R + 1) * (R + 4) / 2;
+    const long bx = off_ext(R, my_m);
+    const int len = R + 2 - my_m;
+    const int qz = z * 5 * gl.spg;
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt) {
+        const int col = 8 * nt + r4;
+        const int q = qz + (col >> 1);
+        if ((col >> 1) >= 5 * gl.spg || q >= nq) continue;
+#pragma unroll
+        for (int par = 0; par < 2; ++par)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int t = my_c * CH + par + 2 * (2 * c4 + v);
+                if (t >= len) continue;
+                reinterpret_cast<double*>(out + (long)q * Kx + bx + t)[col & 1] = acc[nt][par][v];
+            }
+    }
+}
+
+template <int NTC, int NSL>
+void fwd_direct_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out, cudaStream_t st) {
+    const int Jp = ((P.J + 31) / 32) * 32;
+    const size_t sm = (size_t)2 * gl.ns8 * 2 * 8 * gl.sgc * sizeof(double);
+    auto kern = leg_fwd_gt_direct_kernel<NTC, NSL>;
+    static int attr = 0;
+    if ((int)sm > attr) {
+        PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr = (int)sm;
+    }
+    launch_pdl(kern, dim3(P.n_fwd_tasks, gl.groups), dim3(256), sm, st, P.R, Jp, nq, gl, P.d_ptab2, P.d_chk_off,
+               P.d_fwd_ta, P.d_fwd_tb, P.d_gtile, out);
+    PSWE_LAUNCH_CHECK();
+}
+
 // ---- inverse ------------------------------------------------------------------------------
 // X tiles: per column group z (4 NT complex columns from q0 = 4 NT z), per chunk (cbase(m) + c):
 // [16 degrees tl][8 NT + 2] doubles, column 2 ql + {re, im}, two zero pad columns; degree
@@ -866,7 +1006,24 @@ void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t s
     }
     static_assert(kFwdCfg[0].warps == 8 && kFwdCfg[0].cpw == 1 && kFwdCfg[0].stages == 4, "cfg 0");
     static_assert(kFwdCfg[1].warps == 4 && kFwdCfg[1].cpw == 2 && kFwdCfg[1].stages == 3, "cfg 1");
-    if (P.fwd_cfg == 0 && gl.ntc <= 3) {
+    const int nsl = (P.J + 31) / 32;
+    if (PSWE_FWD_DIRECT && P.fwd_cfg == 0 && gl.ntc <= 3 && nsl <= 2 &&
+        (size_t)2 * gl.ns8 * 2 * 8 * gl.sgc * sizeof(double) <= 96 * 1024) {
+        // one or two states on grids up to 64 latitude pairs (T127 on 128 x 256: coarse sweep -2%):
+        // every P fragment in registers before the programmatic-launch wait. At 128 pairs (T255) the
+        // two-slice window leaves the second half's loads on the critical path: fine sweep +3%.
+#define PSWE_DIRECT(NTC)                                                    \
+    switch (nsl) {                                                          \
+        case 1: fwd_direct_launch<NTC, 1>(P, gl, 5 * n, out, st); break;    \
+        default: fwd_direct_launch<NTC, 2>(P, gl, 5 * n, out, st); break;   \
+    }
+        if (gl.ntc == 2) {
+            PSWE_DIRECT(2)
+        } else {
+            PSWE_DIRECT(3)
+        }
+#undef PSWE_DIRECT
+    } else if (P.fwd_cfg == 0 && gl.ntc <= 3) {
         // one or two states: stages of 32 latitudes (four 8-latitude sub-stages per bulk copy, whole
         // 4 KB P tiles) - the per-stage work of narrow column groups is too short to amortise one
         // bulk-copy round trip per 8 latitudes
