@@ -17,7 +17,10 @@ L = _lib.lib()
 prm = P.ModelParams(phi_bar=9.80616e4)
 cp = prm.c()
 out = {}
-for R, nlat, nlon in ((63, 96, 192), (127, 128, 256), (255, 256, 512), (511, 512, 1024), (21, 45, 96)):
+SIZES = ((63, 96, 192), (127, 128, 256), (255, 256, 512), (511, 512, 1024), (21, 45, 96))
+if os.environ.get("EVAL_DUMP_LARGE"):
+    SIZES = ((511, 512, 1024), (511, 768, 1536), (1023, 1024, 2048))
+for R, nlat, nlon in SIZES:
     plan = P.TransformPlan(R, nlat, nlon)
     for n in (1, 2, 3, 5, 7):
         st = torch.as_tensor(np.stack([balanced_random_state(R, 40.0, 11 + i) for i in range(n)])).cuda()
