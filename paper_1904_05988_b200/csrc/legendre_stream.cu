@@ -125,6 +125,31 @@ __global__ void build_ptab2_kernel(int R, int J, int Jp, const double* __restric
     }
 }
 
+// Polar skip table: for order m and 32-latitude slice sl, the first 16-degree chunk whose P tile
+// holds a value of magnitude >= kPolarEps. At high latitudes P^m_s starts from the seed
+// P^m_m ~ (1 - mu^2)^(m/2) and grows with s, so the negligible tiles of a slice are a prefix of its
+// chunks (T511: 17% of all tiles, T1023: 24%). The contractions start there: the skipped terms are
+// < 1e-20 of the normalised P (orthonormal columns), below every double rounding of the sums
+// they would enter (SHTns' "polar optimisation" with a threshold far under the 1e-12 parity bound).
+constexpr double kPolarEps = 1e-20;
+__global__ void build_polar_kernel(int R, int nsl, const int* __restrict__ cbase, const double* __restrict__ ptab,
+                                   int* __restrict__ cstart) {
+    const int sl = blockIdx.x, m = blockIdx.y, lane = threadIdx.x;
+    const int nch = (R + 2 - m + CH - 1) / CH;
+    int first = nch;
+    for (int c = 0; c < nch; ++c) {
+        const double* tile = ptab + ptile_off(cbase[m], nch, nsl, c, sl) + lane * 16;
+        double mx = 0.0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) mx = fmax(mx, fabs(tile[i]));
+        if (__any_sync(0xffffffffu, mx >= kPolarEps)) {
+            first = c;
+            break;
+        }
+    }
+    if (lane == 0) cstart[m * nsl + sl] = first;
+}
+
 template <int NT>
 __device__ __forceinline__ int gpos(int j, int c) {
     if constexpr (NT == 1) return j * 8 + (c ^ (((j >> 1) & 1) << 2));
@@ -423,6 +448,11 @@ __global__ void __launch_bounds__(32 * (W + (PROD ? 1 : 0)), (W == 8 || SUB == 4
     }
 }
 
+// PSWE_NO_POLAR=1 disables the polar skip (A/B and parity checks)
+bool polar_on() {
+    static const bool on = [] { const char* e = getenv("PSWE_NO_POLAR"); return !(e && atoi(e) != 0); }();
+    return on;
+}
 template <int NTC, int W, int CPW, int S, int SUB = 1>
 void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out, cudaStream_t st) {
     const int Jp = ((P.J + 31) / 32) * 32;
@@ -780,7 +810,8 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
                                                              const double* __restrict__ ptab,
                                                              const int* __restrict__ cbase,
                                                              const double* __restrict__ Xt,
-                                                             double2* __restrict__ out) {
+                                                             double2* __restrict__ out,
+                                                             const int* __restrict__ cstart) {
     constexpr int SX = 8 * NT + 2;
     constexpr unsigned PB = 32 * 16 * sizeof(double);
     constexpr unsigned XB = CH * SX * sizeof(double);
@@ -799,8 +830,14 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
     const int nact = min(WS, nsl - sl0);
     const int z = blockIdx.z;
     const int q0 = z * 4 * NT;
-    const double* __restrict__ pm = ptab + ptile_off(cbase[m], nch, nsl, 0, sl0);  // slice sl0 + w: + w nch 512
-    const double* __restrict__ xm = Xt + ((long)z * nct + cbase[m]) * CH * SX;
+    // polar skip: chunks below cs are negligible in every slice of this block
+    int cs = 0;
+    if (cstart) {
+        cs = nch;
+        for (int w = 0; w < nact; ++w) cs = min(cs, cstart[m * nsl + sl0 + w]);
+    }
+    const double* __restrict__ pm = ptab + ptile_off(cbase[m], nch, nsl, cs, sl0);  // slice sl0 + w: + w nch 512
+    const double* __restrict__ xm = Xt + ((long)z * nct + cbase[m] + cs) * CH * SX;
     const int r4 = lane >> 2, c4 = lane & 3;
 
     if (threadIdx.x == 0) {
@@ -812,15 +849,16 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
     }
     __syncthreads();
     pdl_trigger();
-    const int ngr = (nch + CPS - 1) / CPS;  // stages of CPS chunks: one copy per slice, one X copy
+    const int nchs = nch - cs;                // chunks cs .. nch - 1 (indices below relative to cs)
+    const int ngr = (nchs + CPS - 1) / CPS;  // stages of CPS chunks: one copy per slice, one X copy
     auto issue_p = [&](int g) {  // P tiles: plan constants
-        const int k = g % S, c0 = g * CPS, nc = min(CPS, nch - c0);
+        const int k = g % S, c0 = g * CPS, nc = min(CPS, nchs - c0);
         mbar_expect_tx(full + k, nc * (nact * PB + XB));
         for (int w = 0; w < nact; ++w)
             bulk_g2s(sP + (k * WS + w) * CPS * 512, pm + ((long)w * nch + c0) * 512, nc * PB, full + k);
     };
     auto issue_x = [&](int g) {  // X tiles: the prep kernel's output
-        const int k = g % S, c0 = g * CPS, nc = min(CPS, nch - c0);
+        const int k = g % S, c0 = g * CPS, nc = min(CPS, nchs - c0);
         bulk_g2s(sX + k * CPS * CH * SX, xm + (long)c0 * CH * SX, nc * XB, full + k);
     };
     auto issue = [&](int g) {
@@ -849,7 +887,7 @@ __global__ void __launch_bounds__(64 * WS) leg_inv_tma_kernel(int R, int J, int 
     for (int g = 0; g < ngr; ++g) {
         const int k = g % S;
         const unsigned ph = (unsigned)(g / S) & 1u;
-        const int nc = min(CPS, nch - g * CPS);
+        const int nc = min(CPS, nchs - g * CPS);
 #ifndef PSWE_DIAG_NOTMA
         mbar_wait(full + k, ph);
 #endif
@@ -985,7 +1023,7 @@ void inv_tma_launch(const pswe_plan& P, const double* Xt, int nq, double2* out, 
         attr = true;
     }
     launch_pdl(kern, dim3((nsl + WS - 1) / WS, P.R + 1, groups), dim3(64 * WS), sm, st, P.R, P.J, Jp, P.nlat, nq,
-               P.n_chunks, P.d_ptab2, P.d_chk_off, Xt, out);
+               P.n_chunks, P.d_ptab2, P.d_chk_off, Xt, out, (const int*)(polar_on() ? P.d_cstart : nullptr));
     PSWE_LAUNCH_CHECK();
 }
 
@@ -1126,6 +1164,9 @@ void build_legendre_table2(pswe_plan& P) {
     }
     dim3 grid((Jp + 127) / 128, P.R + 1);
     build_ptab2_kernel<<<grid, 128>>>(P.R, P.J, Jp, P.d_mu_n, P.d_seed, P.d_rec, P.d_chk_off, P.d_ptab2);
+    PSWE_LAUNCH_CHECK();
+    PSWE_CUDA(cudaMalloc(&P.d_cstart, (size_t)(P.R + 1) * (Jp / 32) * sizeof(int)));
+    build_polar_kernel<<<dim3(Jp / 32, P.R + 1), 32>>>(P.R, Jp / 32, P.d_chk_off, P.d_ptab2, P.d_cstart);
     PSWE_LAUNCH_CHECK();
 }
 

@@ -117,6 +117,7 @@ struct pswe_plan {
     double2* d_chk = nullptr;    // [sum_m ceil((R+2-m)/16)][J] (P_t, P_{t-1}) at t = 16c (forward DMMA)
     int* d_chk_off = nullptr;    // [R+2] chunk offsets per m into d_chk
     double* d_ptab2 = nullptr;   // STREAM mode: P tiles [m][chunk][Jp][16] swizzled (legendre_stream.cu)
+    int* d_cstart = nullptr;     // STREAM mode: [m][slice] first chunk with |P| >= 1e-20 (polar skip)
     int n_chunks = 0;            // STREAM mode: 16-degree chunks over all m (= d_chk_off[R+1])
     int* d_chunk_m = nullptr;    // STREAM mode: [n_chunks] int2 (order m, chunk within m)
     mutable double* d_xtile = nullptr;  // STREAM mode: inverse X tiles (grow-only scratch)

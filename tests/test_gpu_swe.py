@@ -245,3 +245,21 @@ def test_tile_padding_not_poisoned(P):
     fe5 = host(P.imex_split(cuda(good), p, plan)[1])
     for i in range(5):
         assert rel_diff_fields(fe5[i], O.eval_nonlinear(good[i], po, ref)) < 1e-11
+
+
+def test_polar_skip_bit_identical(tmp_path):
+    """The inverse contraction starts each (order, 32-latitude slice) at the first chunk whose P
+    values reach 1e-20 (polar skip); the evaluations must give the same bits as without it
+    (PSWE_NO_POLAR=1) at T63 ... T511 for batches of 1, 2, 3, 5 and 7 states."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ("0", "1"):
+        out = tmp_path / f"ev{env}.npz"
+        subprocess.run([sys.executable, os.path.join(root, "tools", "eval_dump.py"), str(out)], check=True,
+                       env={**os.environ, "PSWE_NO_POLAR": env}, timeout=600)
+        outs.append(np.load(out))
+    for k in outs[0].files:
+        np.testing.assert_array_equal(outs[0][k], outs[1][k])
