@@ -281,7 +281,8 @@ __global__ void __launch_bounds__(32 * (W + (PROD ? 1 : 0)), (W == 8 || SUB == 4
                                                            const int4* __restrict__ tasks_a,
                                                            const int2* __restrict__ tasks_b,
                                                            const double* __restrict__ gt,
-                                                           double2* __restrict__ out) {
+                                                           double2* __restrict__ out,
+                                                           const int* __restrict__ cstart) {
     constexpr int NS = W * CPW;  // chunk slots
     extern __shared__ __align__(128) double smem[];
     __shared__ long pbase[NS], pstride[NS];  // tile (chunk, slice 0) offset; per-slice stride
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(32 * (W + (PROD ? 1 : 0)), (W == 8 || SUB == 4
     const int wa = (na + CPW - 1) / CPW;  // warps of order a
     const int z = blockIdx.y;
     const int ns8 = gl.ns8;
-    const int nst = ns8 / SUB;  // stages of 8 SUB latitudes
+    __shared__ int nst_s;
     const bool ord_b = warp >= wa;
     const int my_m = ord_b ? ta.w : ta.x;
     const int my_c0 = ord_b ? tb.x + (warp - wa) * CPW : ta.y + warp * CPW;
@@ -334,9 +335,28 @@ __global__ void __launch_bounds__(32 * (W + (PROD ? 1 : 0)), (W == 8 || SUB == 4
         }
         mbar_fence_init();
     }
+    if (warp == 0) {
+        // polar skip at block granularity: the stages (latitudes) past the last 32-latitude slice in
+        // which any of the task's chunks reaches |P| >= 1e-20 are dropped (lane = slice; a task's
+        // most significant chunk of each order is its last one)
+        const int nsl = Jp >> 5;
+        int nsl_eff = nsl;
+        if (cstart) {
+            const int ca = ta.y + na - 1, cb = tb.x + nb - 1;
+            bool sig = false;
+            if (lane < nsl) {
+                sig = ca >= cstart[ta.x * nsl + lane];
+                if (nb > 0) sig = sig || cb >= cstart[ta.w * nsl + lane];
+            }
+            const unsigned bm = __ballot_sync(0xffffffffu, sig);
+            nsl_eff = 32 - __clz((int)bm);
+        }
+        if (lane == 0) nst_s = (nsl_eff * 4) / SUB;  // ns8 = 4 nsl
+    }
     __syncthreads();
     pdl_trigger();
     const int np = npc;
+    const int nst = nst_s;  // stages of 8 SUB latitudes
     // stage q: latitude rows 8 SUB q .. 8 SUB q + 8 SUB - 1; the P tiles (plan constants) and the G
     // tiles (the grid stage's output) complete on the same mbarrier
     auto issue_p = [&](int q) {
@@ -466,7 +486,7 @@ void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out,
     }
     launch_pdl(kern, dim3(P.n_fwd_tasks, gl.groups), dim3(32 * (W + (PSWE_FWD_PROD ? 1 : 0))), sm, st, P.R, Jp, nq, gl,
                P.d_ptab2, P.d_chk_off,
-               P.d_fwd_ta, P.d_fwd_tb, P.d_gtile, out);
+               P.d_fwd_ta, P.d_fwd_tb, P.d_gtile, out, (const int*)(polar_on() ? P.d_cstart : nullptr));
     PSWE_LAUNCH_CHECK();
 }
 
