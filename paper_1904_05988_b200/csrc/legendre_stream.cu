@@ -271,6 +271,12 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
 // PROD: one extra warp only issues the ring refills (it waits for the compute warps' release of
 // stage q and issues stage q + S), so no compute warp stalls on the slowest one before its next
 // stage (T255 batch 98.3 -> 96.8 us, T511 batch 461 -> 443 us). PSWE_FWD_PROD=0: warp 0 refills.
+// WTASK: forward tasks cut by polar-skip weight (build_legendre_table2); 0 = the earlier
+// equal-chunk cut in pair order m, R-m. Bit-identical; T511 batch forward -3.7%, PFASST
+// config 3 / 4 / 5 -0.7 / -0.9 / -1.5% (tools/ab_time.py on the B200).
+#ifndef PSWE_FWD_WTASK
+#define PSWE_FWD_WTASK 1
+#endif
 #ifndef PSWE_FWD_PROD
 #define PSWE_FWD_PROD 1
 #endif
@@ -1123,17 +1129,40 @@ void build_legendre_table2(pswe_plan& P) {
         for (int c = off[m]; c < off[m + 1]; ++c) cm[c] = make_int2(m, c - off[m]);
     PSWE_CUDA(cudaMalloc(&P.d_chunk_m, cm.size() * sizeof(int2)));
     PSWE_CUDA(cudaMemcpy(P.d_chunk_m, cm.data(), cm.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    dim3 grid((Jp + 127) / 128, P.R + 1);
+    build_ptab2_kernel<<<grid, 128>>>(P.R, P.J, Jp, P.d_mu_n, P.d_seed, P.d_rec, P.d_chk_off, P.d_ptab2);
+    PSWE_LAUNCH_CHECK();
+    PSWE_CUDA(cudaMalloc(&P.d_cstart, (size_t)(P.R + 1) * (Jp / 32) * sizeof(int)));
+    build_polar_kernel<<<dim3(Jp / 32, P.R + 1), 32>>>(P.R, Jp / 32, P.d_chk_off, P.d_ptab2, P.d_cstart);
+    PSWE_LAUNCH_CHECK();
     // forward tasks: all (m, chunk) in pair order m, R-m, m+1, R-m-1, ... (equal work per pair) cut
     // into contiguous runs of at most two orders that fit kFwdWarps warps x kFwdCpw chunk slots
     // (each order's run starts on a warp boundary), about kFwdPerSm runs per SM, so that one wave
     // gives every SM the same work (the triangular per-m work otherwise leaves it ragged)
     {
         std::vector<int2> L;
+#if PSWE_FWD_WTASK
+        // weighted cut: orders ascending (neighbouring orders have similar polar profiles, so a
+        // task's stage count is not set by a far-away order), a chunk's weight = the 32-latitude
+        // slices in which it is significant (the block-level polar skip runs a task for the max
+        // over its chunks), tasks cut at equal (slices x chunks) cost
+        const int nsl = Jp / 32;
+        std::vector<int> cst((size_t)(P.R + 1) * nsl);
+        PSWE_CUDA(cudaMemcpy(cst.data(), P.d_cstart, cst.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        auto wt = [&](int m, int c) {
+            int k = 0;
+            while (k < nsl && c >= cst[(size_t)m * nsl + k]) ++k;
+            return std::max(k, 1);
+        };
+        for (int m = 0; m <= P.R; ++m)
+            for (int c = 0; c < off[m + 1] - off[m]; ++c) L.push_back(make_int2(m, c));
+#else
         for (int p = 0; p <= P.R - p; ++p) {
             const int ms[2] = {p, P.R - p};
             for (int u = 0; u < (ms[1] != ms[0] ? 2 : 1); ++u)
                 for (int c = 0; c < off[ms[u] + 1] - off[ms[u]]; ++c) L.push_back(make_int2(ms[u], c));
         }
+#endif
         int nsm = 148;
         {
             int dev = 0;
@@ -1147,7 +1176,13 @@ void build_legendre_table2(pswe_plan& P) {
         auto used = [cpw](int na, int nb) { return (na + cpw - 1) / cpw * cpw + nb; };
         std::vector<int4> ta;
         std::vector<int2> tb;
+#if PSWE_FWD_WTASK
+        long wsum = 0;
+        for (const int2& e : L) wsum += wt(e.x, e.y);
+        for (long target = std::max(1L, (wsum + slots - 1) / slots);; target += std::max(1L, target / 64)) {
+#else
         for (int target = std::max(1, (int)((L.size() + slots - 1) / slots));; ++target) {
+#endif
             ta.clear();
             tb.clear();
             size_t i = 0;
@@ -1155,7 +1190,18 @@ void build_legendre_table2(pswe_plan& P) {
                 int4 a = make_int4(L[i].x, L[i].y, 0, -1);
                 int2 b = make_int2(0, 0);
                 int n = 0;
+#if PSWE_FWD_WTASK
+                int wmax = 0;
+                auto fits = [&](size_t k) {
+                    if (n == 0) return true;
+                    const long w = std::max(wmax, wt(L[k].x, L[k].y));
+                    return n < cap && w * (n + 1) <= target;
+                };
+                while (i < L.size() && fits(i)) {
+                    wmax = std::max(wmax, wt(L[i].x, L[i].y));
+#else
                 while (i < L.size() && n < std::min(target, cap)) {
+#endif
                     if (L[i].x == a.x && a.w < 0) {
                         ++a.z;
                     } else if ((a.w < 0 || L[i].x == a.w) && used(a.z, b.y + 1) <= cap) {
@@ -1174,7 +1220,11 @@ void build_legendre_table2(pswe_plan& P) {
                 ta.push_back(a);
                 tb.push_back(b);
             }
+#if PSWE_FWD_WTASK
+            if ((int)ta.size() <= slots || target >= (long)cap * nsl) break;
+#else
             if ((int)ta.size() <= slots || target >= cap) break;
+#endif
         }
         P.n_fwd_tasks = (int)ta.size();
         PSWE_CUDA(cudaMalloc(&P.d_fwd_ta, ta.size() * sizeof(int4)));
@@ -1182,12 +1232,6 @@ void build_legendre_table2(pswe_plan& P) {
         PSWE_CUDA(cudaMemcpy(P.d_fwd_ta, ta.data(), ta.size() * sizeof(int4), cudaMemcpyHostToDevice));
         PSWE_CUDA(cudaMemcpy(P.d_fwd_tb, tb.data(), tb.size() * sizeof(int2), cudaMemcpyHostToDevice));
     }
-    dim3 grid((Jp + 127) / 128, P.R + 1);
-    build_ptab2_kernel<<<grid, 128>>>(P.R, P.J, Jp, P.d_mu_n, P.d_seed, P.d_rec, P.d_chk_off, P.d_ptab2);
-    PSWE_LAUNCH_CHECK();
-    PSWE_CUDA(cudaMalloc(&P.d_cstart, (size_t)(P.R + 1) * (Jp / 32) * sizeof(int)));
-    build_polar_kernel<<<dim3(Jp / 32, P.R + 1), 32>>>(P.R, Jp / 32, P.d_chk_off, P.d_ptab2, P.d_cstart);
-    PSWE_LAUNCH_CHECK();
 }
 
 void legendre_forward_stream(const pswe_plan& P, const double2* four, int nq, double2* out, bool ext, cudaStream_t st) {
