@@ -274,6 +274,9 @@ __global__ void __launch_bounds__(256) leg_fwd_stream_mma_kernel(int R, int J, i
 // WTASK: forward tasks cut by polar-skip weight (build_legendre_table2); 0 = the earlier
 // equal-chunk cut in pair order m, R-m. Bit-identical; T511 batch forward -3.7%, PFASST
 // config 3 / 4 / 5 -0.7 / -0.9 / -1.5% (tools/ab_time.py on the B200).
+#ifndef PSWE_FWD_WG
+#define PSWE_FWD_WG 0  // per-stage G-tile cost of a task in chunk units (cut cost model)
+#endif
 #ifndef PSWE_FWD_WTASK
 #define PSWE_FWD_WTASK 1
 #endif
@@ -1179,6 +1182,7 @@ void build_legendre_table2(pswe_plan& P) {
 #if PSWE_FWD_WTASK
         long wsum = 0;
         for (const int2& e : L) wsum += wt(e.x, e.y);
+        wsum += (long)PSWE_FWD_WG * slots * nsl / 2;  // per-task stage overhead (G tile) in chunk units
         for (long target = std::max(1L, (wsum + slots - 1) / slots);; target += std::max(1L, target / 64)) {
 #else
         for (int target = std::max(1, (int)((L.size() + slots - 1) / slots));; ++target) {
@@ -1195,7 +1199,7 @@ void build_legendre_table2(pswe_plan& P) {
                 auto fits = [&](size_t k) {
                     if (n == 0) return true;
                     const long w = std::max(wmax, wt(L[k].x, L[k].y));
-                    return n < cap && w * (n + 1) <= target;
+                    return n < cap && w * (n + 1 + PSWE_FWD_WG) <= target;
                 };
                 while (i < L.size() && fits(i)) {
                     wmax = std::max(wmax, wt(L[i].x, L[i].y));
