@@ -724,15 +724,13 @@ __global__ void __launch_bounds__(CH * kPrepItems)
             v[o] = make_double2(inv_a * (-m * chi.y - cpsi.x), inv_a * (m * chi.x - cpsi.y));
             v[o + 1] = make_double2(inv_a * (-m * psi.y + cchi.x), inv_a * (m * psi.x + cchi.y));
         }
+        // NQ = 4 NT is a multiple of PER: the item's columns share one group z (one division per
+        // thread instead of one per column - the divisions were 1/4 of the kernel's instructions)
+        const int q0 = item * PER, z = q0 / NQ, ql0 = q0 - z * NQ;
+        double* row = Xt + ((long)z * nct + cg) * CH * SX + (long)tl * SX + 2 * ql0;
 #pragma unroll
-        for (int f = 0; f < PER; ++f) {
-            const int q = item * PER + f;
-            if (q < nq) {
-                const int z = q / NQ, ql = q - z * NQ;
-                double* row = Xt + ((long)z * nct + cg) * CH * SX + (long)tl * SX;
-                *reinterpret_cast<double2*>(row + 2 * ql) = v[f];
-            }
-        }
+        for (int f = 0; f < PER; ++f)
+            if (q0 + f < nq) *reinterpret_cast<double2*>(row + 2 * f) = v[f];
     }
     for (int z = blockIdx.y * kPrepItems + il; z < groups; z += gridDim.y * kPrepItems) {
         double* row = Xt + ((long)z * nct + cg) * CH * SX + (long)tl * SX;
