@@ -60,6 +60,32 @@ def test_eval_vs_numpy_oracle(P, R, grid):
     assert rel_diff_fields(mine, O.eval_nonlinear(st, po, ref)) < 1e-11
 
 
+@pytest.mark.parametrize("R,grid", [(511, (512, 1024))])
+def test_large_grid_eval_vs_numpy_oracle(P, R, grid):
+    """T511 on BASELINE config 4's 512x1024 grid: the large-grid forward configuration (4-warp
+    tasks, 2 chunks per warp, cut by polar-skip weight) and the single-state one, both against the
+    oracle - the batch-vs-single test alone would not see a chunk the shared task table dropped."""
+    plan = P.TransformPlan(R, grid[0], grid[1])
+    ref = O.TransformPlan(R, grid[0], grid[1])
+    p = P.ModelParams(phi_bar=9.80616 * 1e4)
+    po = O.ModelParams(phi_bar=p.phi_bar)
+    _, ss = fx.degree_order(R)
+    sts = []
+    for seed in (7, 8, 9, 10, 11):
+        st = fx.random_state(R, seed, 1e3, 1e-5) * (ss + 1.0) ** -1.5
+        st[0, 0] = p.phi_bar * math.sqrt(2.0)
+        st[1:, 0] = 0
+        sts.append(st)
+    sts = np.stack(sts)
+    # tolerance: the north star's 1e-10 for spectral coefficients (T511's sums are twice T255's
+    # length; measured 1.1e-11) - a dropped or doubled chunk would show as O(1)
+    batch = host(P.imex_split(cuda(sts), p, plan)[1])
+    for i in (0, 4):
+        want = O.eval_nonlinear(sts[i], po, ref)
+        assert rel_diff_fields(batch[i], want) < 1e-10
+        assert rel_diff_fields(host(P.eval_nonlinear(cuda(sts[i]), p, plan)), want) < 1e-10
+
+
 def test_batched_equals_single(P):
     R = 31
     plan = P.TransformPlan(R)
