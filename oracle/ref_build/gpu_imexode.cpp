@@ -7,8 +7,13 @@
 // oracle/_ref/libpintswe_gpu.so (oracle/build_ref.sh) and driven by tests/test_gpu_dropin.py.
 // Every call copies the state host->device and the result back (the by-value contract of
 // ImexOde); the production path keeps states resident on the device (pswe_level / pswe_pfasst).
+// Thread safety: the reference shares one ImexOde between its PFASST worker threads
+// (Mode::threaded, pfasst.cpp:219-234, runner.cpp:143-144), while a pswe_plan and the adapter's
+// staging buffers are single-stream; every method therefore holds the adapter's mutex across
+// upload, evaluation and download (tests/test_gpu_dropin.py runs the threaded mode).
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -44,16 +49,19 @@ public:
     }
     int truncation() const override { return R_; }
     PrognosticState eval_implicit(const PrognosticState& s) const override {
+        std::lock_guard<std::mutex> lock(mu_);
         upload(s);
         ck(pswe_eval_implicit(R_, &prm_, (const double*)d_in_, (double*)d_out_, 1, nullptr));
         return download();
     }
     PrognosticState eval_explicit(const PrognosticState& s) const override {
+        std::lock_guard<std::mutex> lock(mu_);
         upload(s);
         ck(pswe_eval_explicit(plan_, &prm_, (const double*)d_in_, (double*)d_out_, 1, nullptr));
         return download();
     }
     PrognosticState solve_implicit(const PrognosticState& b, double c) const override {
+        std::lock_guard<std::mutex> lock(mu_);
         upload(b);
         ck(pswe_solve_implicit(R_, &prm_, (const double*)d_in_, c, (double*)d_out_, 1, nullptr));
         return download();
@@ -79,6 +87,7 @@ private:
         std::memcpy(s.div.data(), h.data() + 4 * K, 16 * K);
         return s;
     }
+    mutable std::mutex mu_;
     int R_;
     pswe_params prm_{};
     pswe_plan* plan_ = nullptr;
@@ -148,9 +157,9 @@ int gpuref_sdc_run(int R, int nlat, int nlon, const Params* prm, int nodes, int 
 }
 
 // reference pf::run_block (pfasst.cpp:194-251) in serial emulation with B200 right-hand sides
-int gpuref_pfasst_run(int Rf, int nlat_f, int nlon_f, int Rc, int nlat_c, int nlon_c, const Params* prm, int nodes_f,
-                      int nodes_c, int n_ts, double dt, int n_iter, int n_blocks, const double* theta0,
-                      double* final_state, double* residuals) {
+int gpuref_pfasst_run_mode(int Rf, int nlat_f, int nlon_f, int Rc, int nlat_c, int nlon_c, const Params* prm,
+                           int nodes_f, int nodes_c, int n_ts, double dt, int n_iter, int n_blocks,
+                           const double* theta0, double* final_state, double* residuals, int threaded) {
     return guard([&] {
         const ModelParams m = mp(prm);
         auto fo = std::make_shared<GpuImexOde>(Rf, nlat_f, nlon_f, m);
@@ -165,13 +174,21 @@ int gpuref_pfasst_run(int Rf, int nlat_f, int nlon_f, int Rc, int nlat_c, int nl
         PrognosticState s = state_in(Rf, theta0);
         std::size_t ri = 0;
         for (int b = 0; b < n_blocks; ++b) {
-            pf::BlockResult br = pf::run_block(block, s, pf::Mode::serial_emulation);
+            pf::BlockResult br =
+                pf::run_block(block, s, threaded ? pf::Mode::threaded : pf::Mode::serial_emulation);
             s = br.step_final.back();
             for (const auto& wr : br.residuals)
                 for (double r : wr) residuals[ri++] = r;
         }
         state_out(s, final_state);
     });
+}
+
+int gpuref_pfasst_run(int Rf, int nlat_f, int nlon_f, int Rc, int nlat_c, int nlon_c, const Params* prm, int nodes_f,
+                      int nodes_c, int n_ts, double dt, int n_iter, int n_blocks, const double* theta0,
+                      double* final_state, double* residuals) {
+    return gpuref_pfasst_run_mode(Rf, nlat_f, nlon_f, Rc, nlat_c, nlon_c, prm, nodes_f, nodes_c, n_ts, dt, n_iter,
+                                  n_blocks, theta0, final_state, residuals, 0);
 }
 
 }  // extern "C"

@@ -1250,6 +1250,7 @@ void xtile_reserve(const pswe_plan& P, int nq, int kind) {
     const int groups = (nq + NQ - 1) / NQ;
     const size_t need = (size_t)groups * P.n_chunks * CH * SX;
     if (need > P.xtile_cap) {
+        ++P.generation;
         if (P.d_xtile) PSWE_CUDA(cudaFree(P.d_xtile));
         PSWE_CUDA(cudaMalloc(&P.d_xtile, need * sizeof(double)));
         P.xtile_cap = need;
@@ -1280,10 +1281,10 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
     const int iy = (span + kPrepItems - 1) / kPrepItems;
     const int ipb = std::min(span, kPrepItems);
     dim3 g(P.n_chunks, iy);
+    static const int rows_max = [] { const char* e = getenv("PSWE_PREP_ROWS_MAX"); return e ? atoi(e) : 2; }();
 #ifdef PSWE_DIAG_NOPREP
     if (false)
 #endif
-    static const int rows_max = [] { const char* e = getenv("PSWE_PREP_ROWS_MAX"); return e ? atoi(e) : 2; }();
     if (kind == INV_EVAL && PSWE_PREP_ROWS && NT <= rows_max) {  // env: tuning only
         const dim3 gr((P.n_chunks + kPrepRowChunks - 1) / kPrepRowChunks, groups);
         const int n = nq / 4;

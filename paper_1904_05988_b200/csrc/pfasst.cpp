@@ -293,6 +293,7 @@ struct pswe_pfasst {
     int eager_runs = 0;
     double2* d_theta = nullptr;
     cudaGraphExec_t graph = nullptr;
+    unsigned long long graph_gen = 0;  // plan scratch generations the graph was captured over
     cudaStream_t gstream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
 };
@@ -300,6 +301,13 @@ struct pswe_pfasst {
 namespace {
 
 size_t state_bytes(long K) { return (size_t)3 * K * sizeof(double2); }
+
+// sum of the scratch generations of every level's plan (each only grows)
+unsigned long long plans_generation(const pswe_pfasst* pf) {
+    unsigned long long g = pf->fine->plan->generation + 3 * pf->coarse->plan->generation;
+    if (pf->mid) g += 9 * pf->mid->plan->generation;
+    return g;
+}
 
 void init_common(pswe_pfasst* pf, pswe_pair* pair, const pswe_block_config* cfg, pswe_pair* pair2 = nullptr) {
     if (!pair || !cfg) throw std::invalid_argument("pswe_pfasst: NULL argument");
@@ -648,6 +656,16 @@ int pswe_pfasst_run_block(pswe_pfasst* pf, const double* theta0, double* final_s
                     PSWE_CUDA(cudaEventCreateWithFlags(&pf->ev_out, cudaEventDisableTiming));
                 }
                 const cudaStream_t gs = pf->gstream;
+                // the graph holds raw pointers into the levels' plan scratch, which is grow-only
+                // and reallocated by a larger eval/transform batch, pswe_plan_reserve or a level
+                // with more nodes: any change since the capture makes it stale -> run eagerly once
+                // (re-sizing every pool), then capture again
+                const unsigned long long gen = plans_generation(pf);
+                if (pf->graph && gen != pf->graph_gen) {
+                    PSWE_CUDA(cudaGraphExecDestroy(pf->graph));
+                    pf->graph = nullptr;
+                    pf->eager_runs = 0;
+                }
                 PSWE_CUDA(cudaMemcpyAsync(pf->d_theta, th, state_bytes(pf->Kf), cudaMemcpyDeviceToDevice, st));
                 PSWE_CUDA(cudaEventRecord(pf->ev_in, st));
                 PSWE_CUDA(cudaStreamWaitEvent(gs, pf->ev_in, 0));
@@ -664,6 +682,7 @@ int pswe_pfasst_run_block(pswe_pfasst* pf, const double* theta0, double* final_s
                     PSWE_CUDA(cudaStreamEndCapture(gs, &g));
                     PSWE_CUDA(cudaGraphInstantiate(&pf->graph, g, 0));
                     cudaGraphDestroy(g);
+                    pf->graph_gen = plans_generation(pf);
                 }
                 if (pf->graph) {
                     PSWE_CUDA(cudaGraphLaunch(pf->graph, gs));

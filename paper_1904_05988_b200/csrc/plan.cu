@@ -125,6 +125,7 @@ void pswe_plan::reserve(int batch) {
     if (batch <= cap_batch) return;
     PSWE_CUDA(cudaSetDevice(device));
     // grow-only; callers must not resize during graph capture (pswe_plan_reserve first)
+    ++generation;
     if (d_four_a) cudaFree(d_four_a);
     if (d_four_b) cudaFree(d_four_b);
     if (d_proj) cudaFree(d_proj);

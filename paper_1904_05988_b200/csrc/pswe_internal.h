@@ -144,6 +144,9 @@ struct pswe_plan {
     double2* d_four_b = nullptr;  // [cap * 5 * (R+1) * nlat]
     double2* d_proj = nullptr;    // [cap * 5 * Kx] Legendre projections, extended layout
     double2* d_xcoef = nullptr;   // [cap * 5 * Kx] inverse-Legendre coefficients (U/V derived), ext layout
+    // bumped on every scratch reallocation: a CUDA graph captured over this plan's scratch
+    // (pswe_pfasst's serial-emulation block) is stale once it changes
+    mutable unsigned long long generation = 0;
     void reserve(int batch);
 };
 

@@ -47,6 +47,7 @@ def gref():
     L.gpuref_last_error.restype = ctypes.c_char_p
     L.gpuref_sdc_run.argtypes = [ci, ci, ci, vp, ci, ci, cd, ci, vp, vp, vp]
     L.gpuref_pfasst_run.argtypes = [ci] * 6 + [vp, ci, ci, ci, cd, ci, ci, vp, vp, vp]
+    L.gpuref_pfasst_run_mode.argtypes = [ci] * 6 + [vp, ci, ci, ci, cd, ci, ci, vp, vp, vp, ci]
     return L
 
 
@@ -72,6 +73,21 @@ def test_reference_pfasst_on_gpu_rhs(gref, golden):
     prm = ref.Params(6.37122e6, 7.292e-5, 9.80616, PHI_BAR, 0.0)
     rc = gref.gpuref_pfasst_run(31, 0, 0, 15, 0, 0, ctypes.byref(prm), 5, 3, 4, 60.0, 3, 1, _p(th), _p(fin),
                                 _p(res))
+    assert rc == 0, gref.gpuref_last_error()
+    assert rel_diff_fields(fin, golden["pf_nts4_final"]) < 1e-10
+    assert res_ok(res, golden["pf_nts4_res"], fin)
+
+
+def test_reference_pfasst_threaded_on_gpu_rhs(gref, golden):
+    """The reference's Mode::threaded (one std::thread per worker, pfasst.cpp:219-234) sharing ONE
+    GpuImexOde between the 4 workers (runner.cpp:143-144): the adapter serialises its calls, and
+    the block reproduces the serial reference result."""
+    th = np.ascontiguousarray(golden["pf_theta0"])
+    fin = np.zeros_like(th)
+    res = np.zeros((1, 4, 4))
+    prm = ref.Params(6.37122e6, 7.292e-5, 9.80616, PHI_BAR, 0.0)
+    rc = gref.gpuref_pfasst_run_mode(31, 0, 0, 15, 0, 0, ctypes.byref(prm), 5, 3, 4, 60.0, 3, 1, _p(th), _p(fin),
+                                     _p(res), 1)
     assert rc == 0, gref.gpuref_last_error()
     assert rel_diff_fields(fin, golden["pf_nts4_final"]) < 1e-10
     assert res_ok(res, golden["pf_nts4_res"], fin)

@@ -61,14 +61,18 @@ def test_eval_vs_numpy_oracle(P, R, grid):
 
 
 @pytest.mark.parametrize("R,grid", [(511, (512, 1024))])
-def test_large_grid_eval_vs_numpy_oracle(P, R, grid):
+def test_large_grid_eval_vs_reference(P, R, grid):
     """T511 on BASELINE config 4's 512x1024 grid: the large-grid forward configuration (4-warp
     tasks, 2 chunks per warp, cut by polar-skip weight) and the single-state one, both against the
-    oracle - the batch-vs-single test alone would not see a chunk the shared task table dropped."""
+    REFERENCE (oracle/_ref) at 1e-11 per field - the batch-vs-single test alone would not see a chunk
+    the shared task table dropped. (Round 1 compared with the numpy restatement at 1e-10: that
+    restatement itself sits 1.3e-11 from the reference here, tests/test_oracle_golden.py.)"""
+    from oracle import ref_lib as ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
     plan = P.TransformPlan(R, grid[0], grid[1])
-    ref = O.TransformPlan(R, grid[0], grid[1])
+    rp = ref.RefPlan(R, grid[0], grid[1])
     p = P.ModelParams(phi_bar=9.80616 * 1e4)
-    po = O.ModelParams(phi_bar=p.phi_bar)
     _, ss = fx.degree_order(R)
     sts = []
     for seed in (7, 8, 9, 10, 11):
@@ -77,13 +81,11 @@ def test_large_grid_eval_vs_numpy_oracle(P, R, grid):
         st[1:, 0] = 0
         sts.append(st)
     sts = np.stack(sts)
-    # tolerance: the north star's 1e-10 for spectral coefficients (T511's sums are twice T255's
-    # length; measured 1.1e-11) - a dropped or doubled chunk would show as O(1)
     batch = host(P.imex_split(cuda(sts), p, plan)[1])
     for i in (0, 4):
-        want = O.eval_nonlinear(sts[i], po, ref)
-        assert rel_diff_fields(batch[i], want) < 1e-10
-        assert rel_diff_fields(host(P.eval_nonlinear(cuda(sts[i]), p, plan)), want) < 1e-10
+        want = rp.eval_nonlinear(sts[i], p)
+        assert rel_diff_fields(batch[i], want) < 1e-11
+        assert rel_diff_fields(host(P.eval_nonlinear(cuda(sts[i]), p, plan)), want) < 1e-11
 
 
 def test_batched_equals_single(P):
