@@ -538,9 +538,10 @@ def run_pfasst(P, prm, world, rank, dev, clocks_dev=0, config=3):
     if world == 1:
         pf = P.Pfasst(pair, cfg, pair2=pair2)
     else:
-        uid = [P.pfasst.nccl_unique_id() if rank == 0 else None]
+        transport = os.environ.get("PSWE_TRANSPORT", "ipc")  # CUDA IPC over NVLink (default) or "nccl"
+        uid = [P.pfasst.unique_id(transport) if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        pf = P.Pfasst(pair, cfg, rank=rank, world=world, nccl_id=uid[0], pair2=pair2)
+        pf = P.Pfasst(pair, cfg, rank=rank, world=world, uid=uid[0], pair2=pair2, transport=transport)
     theta0 = torch.as_tensor(config_state(config, plans[0])).to(dev)
     P.run_blocks(pf, theta0, 1)  # warm-up block (also captures the serial-emulation graph)
     torch.cuda.synchronize()

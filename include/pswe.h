@@ -171,6 +171,24 @@ int pswe_pfasst_create_serial(pswe_pair* pair, const pswe_block_config* cfg, psw
 int pswe_pfasst_create_nccl(pswe_pair* pair, const pswe_block_config* cfg, int rank, int world,
                             const void* nccl_unique_id, pswe_pfasst** out);
 int pswe_nccl_unique_id(void* out128);
+/* Distributed controller over a chosen message transport (one process per GPU, rank = worker):
+ *   PSWE_TRANSPORT_IPC  — CUDA IPC over peer memory (NVLink/NVSwitch within one node; several
+ *                         processes may share one GPU): the sender's kernel writes each message
+ *                         into the receiver's ring slot, a POSIX shared-memory segment named by the
+ *                         unique id carries counters, handles, a barrier and the abort flag;
+ *   PSWE_TRANSPORT_NCCL — ncclSend/ncclRecv (two communicators per level by sender parity).
+ * mid_coarse = NULL for two levels. unique_id: 128 bytes from pswe_transport_unique_id on rank 0,
+ * shared by the caller. Every message carries a (phase, iteration, level, sender, sequence) tag
+ * checked on receipt ("pfasst: message tag mismatch", pfasst.cpp:71-76); every wait is bounded by
+ * the receive timeout (BlockConfig::recv_timeout_seconds, pfasst.hpp:19; default 300 s, env
+ * PSWE_RECV_TIMEOUT) and fails with "pfasst: receive timed out, pipeline deadlock suspected"
+ * (pfasst.cpp:39-47); a rank whose block fails aborts the block for its peers. */
+#define PSWE_TRANSPORT_NCCL 0
+#define PSWE_TRANSPORT_IPC 1
+int pswe_transport_unique_id(int transport, void* out128);
+int pswe_pfasst_create_dist(pswe_pair* pair, pswe_pair* mid_coarse, const pswe_block_config* cfg, int rank,
+                            int world, int transport, const void* unique_id, pswe_pfasst** out);
+int pswe_pfasst_set_recv_timeout(pswe_pfasst* pf, double seconds);
 /* Three-level PFASST (BASELINE config 4; the reference implements two levels only,
  * multilevel.hpp:29-35): fine_mid = (fine, mid), mid_coarse = (mid, coarse) with
  * mid_coarse->fine == fine_mid->coarse. Each iteration is a V-cycle fine -> mid -> coarse -> mid
@@ -188,6 +206,10 @@ int pswe_pfasst_destroy(pswe_pfasst* pf);
  *                         gathered to every rank. */
 int pswe_pfasst_run_block(pswe_pfasst* pf, const double* theta0, double* final_state, double* residuals,
                           void* stream);
+/* The same with BlockResult.step_final (pfasst.hpp:34-36): step_final (device, n_time_steps
+ * states, may be NULL) receives the fine last-node state of every time step of the block. */
+int pswe_pfasst_run_block_steps(pswe_pfasst* pf, const double* theta0, double* step_final, double* final_state,
+                                double* residuals, void* stream);
 /* Message log of the last block (pfasst.hpp:22-31), 7 ints per record:
  * phase, iteration, step ('B','P','A','C'), sender, receiver, level, node. Returns the count. */
 int pswe_pfasst_messages(const pswe_pfasst* pf, int* out, int max_records);

@@ -77,6 +77,10 @@ SIGNATURES = {
     "pswe_pfasst3_create_serial": (_i, [_vp, _vp, ctypes.POINTER(BlockConfig), ctypes.POINTER(_vp)]),
     "pswe_pfasst3_create_nccl": (_i, [_vp, _vp, ctypes.POINTER(BlockConfig), _i, _i, _vp, ctypes.POINTER(_vp)]),
     "pswe_nccl_unique_id": (_i, [_vp]),
+    "pswe_transport_unique_id": (_i, [_i, _vp]),
+    "pswe_pfasst_create_dist": (_i, [_vp, _vp, ctypes.POINTER(BlockConfig), _i, _i, _i, _vp, ctypes.POINTER(_vp)]),
+    "pswe_pfasst_set_recv_timeout": (_i, [_vp, _d]),
+    "pswe_pfasst_run_block_steps": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_pfasst_destroy": (_i, [_vp]),
     "pswe_pfasst_run_block": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "pswe_pfasst_messages": (_i, [_vp, _pi, _i]),

@@ -5,13 +5,14 @@
 // worker_predict :78-120 and worker_iterate :122-176 op for op) and executed by
 //   * SerialExec  — all workers on this GPU in worker order with in-process message queues
 //                   (the reference's Mode::serial_emulation, :212-216);
-//   * NcclExec    — one process per GPU, worker w = rank, messages carried by NCCL send/recv
-//                   over NVLink. The reference's two forward-only channels (fine_ch/coarse_ch,
-//                   :65-66) become two NCCL communicators per direction parity: rank w sends on
-//                   comm[level][w%2] from a dedicated send stream (the reference's send never
-//                   blocks, :31-37) and receives on comm[level][(w+1)%2] on the compute stream,
-//                   so no communicator is ever used from two streams and sends can never block
-//                   the compute pipeline (which would deadlock Step C against Step A).
+//   * run_dist    — one process per GPU, worker w = rank, messages through a Transport
+//                   (transport.h): CUDA IPC over peer memory (NVLink/NVSwitch; also several
+//                   processes on one GPU) or NCCL send/recv. Every message carries a
+//                   (phase, iteration, level, sender, sequence) trailer checked on receipt
+//                   (the reference's expect(), :71-76), receives are bounded by
+//                   recv_timeout_seconds (pfasst.hpp:19, :39-47) and a failing rank aborts
+//                   the block for its peers (the reference rethrows worker exceptions,
+//                   :219-234).
 // The same schedule is exported through pswe_pfasst_schedule() so the multi-rank host logic is
 // tested on CPU with gloo (tests/test_pfasst_schedule.py).
 #include <dlfcn.h>
@@ -25,6 +26,7 @@
 #include <tuple>
 
 #include "pswe_internal.h"
+#include "transport.h"
 
 namespace pswe {
 void level_spread(pswe_level* L, const double2* theta0, cudaStream_t st);
@@ -200,56 +202,6 @@ std::vector<MsgRec> message_log(int n, int n_iter, int mf, int mc, int nlev = 2,
     return log;
 }
 
-// ---- NCCL (resolved at run time so libpswe.so loads on machines without NCCL) --------------
-
-typedef struct ncclComm* ncclComm_t;
-typedef struct {
-    char internal[128];
-} ncclUniqueId;
-enum { ncclFloat64 = 8, ncclUint8 = 1 };
-typedef int ncclResult_t;
-
-struct NcclApi {
-    void* h = nullptr;
-    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*Broadcast)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    const char* (*GetErrorString)(ncclResult_t) = nullptr;
-    void load() {
-        if (h) return;
-        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-            h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
-            if (h) break;
-        }
-        if (!h) throw std::runtime_error("NCCL not available (dlopen libnccl.so.2 failed)");
-        auto sym = [&](const char* s) {
-            void* p = dlsym(h, s);
-            if (!p) throw std::runtime_error(std::string("NCCL symbol missing: ") + s);
-            return p;
-        };
-        GetUniqueId = (decltype(GetUniqueId))sym("ncclGetUniqueId");
-        CommInitRank = (decltype(CommInitRank))sym("ncclCommInitRank");
-        CommDestroy = (decltype(CommDestroy))sym("ncclCommDestroy");
-        Send = (decltype(Send))sym("ncclSend");
-        Recv = (decltype(Recv))sym("ncclRecv");
-        Broadcast = (decltype(Broadcast))sym("ncclBroadcast");
-        AllGather = (decltype(AllGather))sym("ncclAllGather");
-        GetErrorString = (decltype(GetErrorString))sym("ncclGetErrorString");
-    }
-    void check(ncclResult_t r, const char* what) const {
-        if (r != 0) throw std::runtime_error(std::string(what) + ": " + GetErrorString(r));
-    }
-};
-static NcclApi& nccl() {
-    static NcclApi api;
-    api.load();
-    return api;
-}
-
 }  // namespace pswe
 
 using namespace pswe;
@@ -278,15 +230,17 @@ struct pswe_pfasst {
     };
     std::map<std::pair<int, int>, std::deque<Msg>> queues;
     std::vector<double2*> pool[3];  // free message buffers per level
-    // NCCL
-    ncclComm_t comm[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};  // [level][parity]
-    ncclComm_t world_comm = nullptr;
-    cudaStream_t send_stream[3] = {nullptr, nullptr, nullptr};
-    std::vector<double2*> send_bufs[3];
-    std::vector<cudaEvent_t> send_done[3];
-    size_t send_next[3] = {0, 0, 0};
+    // distributed: this rank's worker, messages through the transport
+    std::unique_ptr<Transport> tr;
+    unsigned long long sseq[3] = {0, 0, 0}, rseq[3] = {0, 0, 0};  // messages sent / received per level
+    TagError* h_err = nullptr;  // host-mapped: raised by consume kernels on a tag mismatch
+    TagError* d_err = nullptr;
+    double recv_timeout = 300.0;  // BlockConfig::recv_timeout_seconds (pfasst.hpp:19)
+    int fault = 0;                // fault injection for tests (PSWE_PFASST_FAULT): 1 = skew tags
+    bool broken = false;          // a block failed: the transport state is undefined
+    // BlockResult.step_final (pfasst.hpp:34-36): serial: every worker's last fine node [n][3Kf]
+    double2* d_step_final = nullptr;
     long K_of(int level) const { return level == 0 ? Kf : (level == nlev - 1 ? Kc : Km); }
-    double* d_res_all = nullptr;
     // serial emulation replays the whole block as one CUDA graph (captured on the 2nd call,
     // after an eager call has sized every pool); theta0 is copied into d_theta first
     bool use_graph = true;
@@ -457,46 +411,54 @@ void run_serial(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
         if (has_low_replace(pf, level)) replace_low_modes(pf, level, dst, st);
         pf->pool[level].push_back(m.buf);  // stream-ordered reuse
     };
-    for (int w = 0; w < pf->cfg.n_time_steps; ++w) run_worker(pf, w, theta0, st, send, recv);
+    for (int w = 0; w < pf->cfg.n_time_steps; ++w) {
+        run_worker(pf, w, theta0, st, send, recv);
+        // BlockResult.step_final[w] (pfasst.cpp:238-241): the workers share the levels in turn
+        PSWE_CUDA(cudaMemcpyAsync(pf->d_step_final + (size_t)w * 3 * pf->Kf, st_ptr(pf->fine, pf->mf - 1),
+                                  state_bytes(pf->Kf), cudaMemcpyDeviceToDevice, st));
+    }
 }
 
-void run_nccl(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
-    auto& api = nccl();
-    const int w = pf->rank, n = pf->world;
-    auto send = [&](int, int level, int, int, const double2* src, long K) {
-        // stage into a ring buffer (the reference's message holds a copy), then send from the
-        // level's send stream so the compute stream never waits for the receiver
-        const size_t slot = pf->send_next[level]++ % pf->send_bufs[level].size();
-        double2* b = pf->send_bufs[level][slot];
-        cudaEvent_t ev = pf->send_done[level][slot];
-        PSWE_CUDA(cudaStreamWaitEvent(st, ev, 0));  // previous send from this slot finished
-        PSWE_CUDA(cudaMemcpyAsync(b, src, state_bytes(K), cudaMemcpyDeviceToDevice, st));
-        cudaEvent_t ready;
-        PSWE_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-        PSWE_CUDA(cudaEventRecord(ready, st));
-        PSWE_CUDA(cudaStreamWaitEvent(pf->send_stream[level], ready, 0));
-        PSWE_CUDA(cudaEventDestroy(ready));
-        api.check(api.Send(b, state_bytes(K) / sizeof(double), ncclFloat64, w + 1, pf->comm[level][w % 2],
-                           pf->send_stream[level]),
-                  "ncclSend");
-        PSWE_CUDA(cudaEventRecord(ev, pf->send_stream[level]));
+void run_dist(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
+    Transport& T = *pf->tr;
+    const int w = pf->rank;
+    auto tag_of = [&](int level, int phase, int iter, int sender, unsigned long long seq) {
+        MsgTag t{};
+        t.magic = kMsgMagic;
+        t.phase = phase;
+        t.iter = iter;
+        t.level = level;
+        t.sender = sender;
+        t.seq_lo = (int)(seq & 0xffffffffu);
+        t.seq_hi = (int)(seq >> 32);
+        return t;
     };
-    auto recv = [&](int, int level, int, int, double2* dst, long K) {
-        // fine IC: receive into dst, then add the node-0 increment in place (pfasst.cpp:171-174)
-        api.check(api.Recv(dst, state_bytes(K) / sizeof(double), ncclFloat64, w - 1, pf->comm[level][(w + 1) % 2], st),
-                  "ncclRecv");
-        if (has_dstate(pf, level)) add_dstate0(pf, dst, dst, st, level);
+    auto send = [&](int, int level, int phase, int iter, const double2* src, long) {
+        const unsigned long long k = pf->sseq[level]++;
+        // fault injection (tests): the first iteration message carries the wrong iteration
+        const int skew = (pf->fault == 1 && phase == 1 && iter == 1) ? 1 : 0;
+        T.send(level, k, src, tag_of(level, phase, iter + skew, w, k), st);
+    };
+    auto recv = [&](int, int level, int phase, int iter, double2* dst, long K) {
+        const unsigned long long k = pf->rseq[level]++;
+        const double2* slot = T.recv(level, k, st);
+        // copy into place (+ the receiver's node-0 increment for the two-level fine IC,
+        // pfasst.cpp:171-174) and check the trailer (pfasst.cpp:71-76) in one kernel
+        consume_message(dst, slot, has_dstate(pf, level) ? (level ? pf->d_dstate0_mid : pf->d_dstate0) : nullptr,
+                        3 * K, tag_of(level, phase, iter, w - 1, k), pf->d_err, st);
         if (has_low_replace(pf, level)) replace_low_modes(pf, level, dst, st);
     };
     run_worker(pf, w, theta0, st, send, recv);
-    // make sure all sends are posted before the block ends
-    for (int l = 0; l < pf->nlev; ++l) {
-        cudaEvent_t e;
-        PSWE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        PSWE_CUDA(cudaEventRecord(e, pf->send_stream[l]));
-        PSWE_CUDA(cudaStreamWaitEvent(st, e, 0));
-        PSWE_CUDA(cudaEventDestroy(e));
-    }
+}
+
+void check_tags(pswe_pfasst* pf) {
+    if (!pf->h_err || !pf->h_err->flag) return;
+    const TagError e = *pf->h_err;
+    std::memset(pf->h_err, 0, sizeof(TagError));
+    throw std::logic_error("pfasst: message tag mismatch (received phase " + std::to_string(e.phase) + " iteration " +
+                           std::to_string(e.iter) + " level " + std::to_string(e.level) + " from worker " +
+                           std::to_string(e.sender) + ", expected phase " + std::to_string(e.want_phase) +
+                           " iteration " + std::to_string(e.want_iter) + " level " + std::to_string(e.want_level) + ")");
 }
 
 }  // namespace
@@ -509,8 +471,9 @@ static void create_serial(pswe_pair* pair, pswe_pair* pair2, const pswe_block_co
     if (const char* e = std::getenv("PSWE_NO_GRAPH")) pf->use_graph = std::atoi(e) == 0;
     try {
         init_common(pf, pair, cfg, pair2);
+        PSWE_CUDA(cudaMalloc(&pf->d_step_final, pf->cfg.n_time_steps * state_bytes(pf->Kf)));
     } catch (...) {
-        delete pf;
+        pswe_pfasst_destroy(pf);
         throw;
     }
     *out = pf;
@@ -528,74 +491,83 @@ int pswe_pfasst3_create_serial(pswe_pair* fine_mid, pswe_pair* mid_coarse, const
     });
 }
 
-int pswe_nccl_unique_id(void* out128) {
+int pswe_transport_unique_id(int transport, void* out128) {
     return guarded([&] {
-        ncclUniqueId id;
-        nccl().check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
-        std::memcpy(out128, &id, sizeof(id));
+        if (!out128) throw std::invalid_argument("NULL argument");
+        if (transport == PSWE_TRANSPORT_IPC) ipc_unique_id(out128);
+        else if (transport == PSWE_TRANSPORT_NCCL) nccl_unique_id(out128);
+        else throw std::invalid_argument("pswe_transport_unique_id: unknown transport");
     });
 }
 
-static void create_nccl(pswe_pair* pair, pswe_pair* pair2, const pswe_block_config* cfg, int rank, int world,
-                        const void* uid, pswe_pfasst** out) {
-    {
-        if (!out || !uid) throw std::invalid_argument("NULL argument");
-        if (cfg && cfg->n_time_steps != world)
-            throw std::invalid_argument("pswe_pfasst_create_nccl: n_time_steps must equal world size");
-        auto& api = nccl();
-        auto* pf = new pswe_pfasst;
-        init_common(pf, pair, cfg, pair2);
+int pswe_nccl_unique_id(void* out128) { return pswe_transport_unique_id(PSWE_TRANSPORT_NCCL, out128); }
+
+static void create_dist(pswe_pair* pair, pswe_pair* pair2, const pswe_block_config* cfg, int rank, int world,
+                        int transport, const void* uid, pswe_pfasst** out) {
+    if (!out || !uid) throw std::invalid_argument("NULL argument");
+    if (!cfg) throw std::invalid_argument("pswe_pfasst: NULL argument");
+    if (cfg->n_time_steps != world)
+        throw std::invalid_argument("pswe_pfasst_create_dist: n_time_steps must equal world size");
+    if (rank < 0 || rank >= world) throw std::invalid_argument("pswe_pfasst_create_dist: rank out of range");
+    std::unique_ptr<pswe_pfasst> pf(new pswe_pfasst);
+    try {
+        init_common(pf.get(), pair, cfg, pair2);
         pf->distributed = true;
         pf->rank = rank;
         pf->world = world;
-        // 5 communicators from one unique id: derive distinct ids by perturbing a byte the
-        // bootstrap does not use for addressing is not portable, so every comm is initialised
-        // from the same id sequentially (NCCL allows re-using an id once per init round).
-        ncclUniqueId base;
-        std::memcpy(&base, uid, sizeof(base));
-        api.check(api.CommInitRank(&pf->world_comm, world, base, rank), "ncclCommInitRank(world)");
-        for (int l = 0; l < pf->nlev; ++l)
-            for (int p = 0; p < 2; ++p) {
-                // per-comm ids are broadcast through the world communicator
-                ncclUniqueId id;
-                if (rank == 0) api.check(api.GetUniqueId(&id), "ncclGetUniqueId");
-                char* d_id;
-                PSWE_CUDA(cudaMalloc(&d_id, sizeof(id)));
-                PSWE_CUDA(cudaMemcpy(d_id, &id, sizeof(id), cudaMemcpyHostToDevice));
-                api.check(api.Broadcast(d_id, d_id, sizeof(id), ncclUint8, 0, pf->world_comm, 0), "ncclBroadcast(id)");
-                PSWE_CUDA(cudaMemcpy(&id, d_id, sizeof(id), cudaMemcpyDeviceToHost));
-                cudaFree(d_id);
-                api.check(api.CommInitRank(&pf->comm[l][p], world, id, rank), "ncclCommInitRank(p2p)");
-            }
-        for (int l = 0; l < pf->nlev; ++l) {
-            PSWE_CUDA(cudaStreamCreateWithFlags(&pf->send_stream[l], cudaStreamNonBlocking));
-            const long K = pf->K_of(l);
-            const int nslots = l == pf->nlev - 1 ? world + cfg->n_iter + 2 : cfg->n_iter + 2;
-            for (int s = 0; s < nslots; ++s) {
-                double2* b;
-                PSWE_CUDA(cudaMalloc(&b, state_bytes(K)));
-                pf->send_bufs[l].push_back(b);
-                cudaEvent_t e;
-                PSWE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-                PSWE_CUDA(cudaEventRecord(e, pf->send_stream[l]));
-                pf->send_done[l].push_back(e);
-            }
-        }
-        PSWE_CUDA(cudaMalloc(&pf->d_res_all, sizeof(double) * world * (cfg->n_iter + 1)));
-        *out = pf;
+        if (const char* e = std::getenv("PSWE_RECV_TIMEOUT")) pf->recv_timeout = std::atof(e);
+        if (const char* e = std::getenv("PSWE_PFASST_FAULT")) pf->fault = std::atoi(e);
+        PSWE_CUDA(cudaHostAlloc(&pf->h_err, sizeof(TagError), cudaHostAllocMapped));
+        std::memset(pf->h_err, 0, sizeof(TagError));
+        PSWE_CUDA(cudaHostGetDevicePointer(&pf->d_err, pf->h_err, 0));
+        TransportConfig tc;
+        tc.rank = rank;
+        tc.world = world;
+        tc.nlev = pf->nlev;
+        for (int l = 0; l < pf->nlev; ++l) tc.K[l] = pf->K_of(l);
+        // messages per level and receiver within one block: fine / mid <= n_iter - 1, coarse
+        // <= world + n_iter - 1 (prediction rounds + Step C); slots are reused only in the next
+        // block, after the block-end synchronisation
+        tc.slots = world + cfg->n_iter + 1;
+        tc.Kfinal = pf->Kf;
+        tc.n_res = cfg->n_iter + 1;
+        tc.timeout_s = pf->recv_timeout;
+        pf->tr = transport == PSWE_TRANSPORT_IPC ? make_ipc_transport(tc, uid) : make_nccl_transport(tc, uid);
+    } catch (...) {
+        pswe_pfasst_destroy(pf.release());
+        throw;
     }
+    *out = pf.release();
+}
+
+int pswe_pfasst_create_dist(pswe_pair* pair, pswe_pair* mid_coarse, const pswe_block_config* cfg, int rank,
+                            int world, int transport, const void* unique_id, pswe_pfasst** out) {
+    return guarded([&] {
+        if (transport != PSWE_TRANSPORT_IPC && transport != PSWE_TRANSPORT_NCCL)
+            throw std::invalid_argument("pswe_pfasst_create_dist: unknown transport");
+        create_dist(pair, mid_coarse, cfg, rank, world, transport, unique_id, out);
+    });
 }
 
 int pswe_pfasst_create_nccl(pswe_pair* pair, const pswe_block_config* cfg, int rank, int world,
                             const void* uid, pswe_pfasst** out) {
-    return guarded([&] { create_nccl(pair, nullptr, cfg, rank, world, uid, out); });
+    return guarded([&] { create_dist(pair, nullptr, cfg, rank, world, PSWE_TRANSPORT_NCCL, uid, out); });
 }
 
 int pswe_pfasst3_create_nccl(pswe_pair* fine_mid, pswe_pair* mid_coarse, const pswe_block_config* cfg, int rank,
                              int world, const void* uid, pswe_pfasst** out) {
     return guarded([&] {
         if (!mid_coarse) throw std::invalid_argument("pswe_pfasst3: NULL mid-coarse pair");
-        create_nccl(fine_mid, mid_coarse, cfg, rank, world, uid, out);
+        create_dist(fine_mid, mid_coarse, cfg, rank, world, PSWE_TRANSPORT_NCCL, uid, out);
+    });
+}
+
+int pswe_pfasst_set_recv_timeout(pswe_pfasst* pf, double seconds) {
+    return guarded([&] {
+        if (!pf) throw std::invalid_argument("NULL argument");
+        if (!(seconds > 0)) throw std::invalid_argument("pswe_pfasst_set_recv_timeout: need seconds > 0");
+        pf->recv_timeout = seconds;
+        if (pf->tr) pf->tr->timeout_s = seconds;
     });
 }
 
@@ -608,35 +580,27 @@ int pswe_pfasst_destroy(pswe_pfasst* pf) {
         if (pf->gstream) cudaStreamDestroy(pf->gstream);
         if (pf->ev_in) cudaEventDestroy(pf->ev_in);
         if (pf->ev_out) cudaEventDestroy(pf->ev_out);
-        cudaFree(pf->d_tau);
-        cudaFree(pf->d_dstate0);
+        if (pf->d_tau) cudaFree(pf->d_tau);
+        if (pf->d_dstate0) cudaFree(pf->d_dstate0);
         if (pf->d_tau_mid) cudaFree(pf->d_tau_mid);
         if (pf->d_dstate0_mid) cudaFree(pf->d_dstate0_mid);
         cudaFree(pf->d_res);
-        if (pf->d_res_all) cudaFree(pf->d_res_all);
-        for (int l = 0; l < 3; ++l) {
+        if (pf->d_step_final) cudaFree(pf->d_step_final);
+        for (int l = 0; l < 3; ++l)
             for (auto* b : pf->pool[l]) cudaFree(b);
-            for (auto* b : pf->send_bufs[l]) cudaFree(b);
-            for (auto e : pf->send_done[l]) cudaEventDestroy(e);
-            if (pf->send_stream[l]) cudaStreamDestroy(pf->send_stream[l]);
-        }
         for (auto& q : pf->queues)
             for (auto& m : q.second) cudaFree(m.buf);
-        if (pf->distributed) {
-            auto& api = nccl();
-            for (auto& l : pf->comm)
-                for (auto c : l)
-                    if (c) api.CommDestroy(c);
-            if (pf->world_comm) api.CommDestroy(pf->world_comm);
-        }
+        pf->tr.reset();
+        if (pf->h_err) cudaFreeHost(pf->h_err);
         delete pf;
     });
 }
 
-int pswe_pfasst_run_block(pswe_pfasst* pf, const double* theta0, double* final_state, double* residuals,
-                          void* stream) {
+int pswe_pfasst_run_block_steps(pswe_pfasst* pf, const double* theta0, double* step_final, double* final_state,
+                                double* residuals, void* stream) {
     return guarded([&] {
         if (!pf || !theta0) throw std::invalid_argument("NULL argument");
+        if (pf->broken) throw std::runtime_error("pfasst: a previous block failed; destroy and recreate the controller");
         const cudaStream_t st = as_stream(stream);
         const double2* th = reinterpret_cast<const double2*>(theta0);
         const int n = pf->cfg.n_time_steps, N = pf->cfg.n_iter;
@@ -696,32 +660,40 @@ int pswe_pfasst_run_block(pswe_pfasst* pf, const double* theta0, double* final_s
             if (final_state)
                 PSWE_CUDA(cudaMemcpyAsync(final_state, st_ptr(pf->fine, pf->mf - 1), state_bytes(pf->Kf),
                                           cudaMemcpyDeviceToDevice, st));
+            if (step_final)
+                PSWE_CUDA(cudaMemcpyAsync(step_final, pf->d_step_final, n * state_bytes(pf->Kf),
+                                          cudaMemcpyDeviceToDevice, st));
             if (residuals) {
                 PSWE_CUDA(cudaMemcpyAsync(residuals, pf->d_res, sizeof(double) * n * (N + 1), cudaMemcpyDeviceToHost, st));
                 PSWE_CUDA(cudaStreamSynchronize(st));
             }
         } else {
-            auto& api = nccl();
-            run_nccl(pf, th, st);
             // BlockResult: the last step's final state goes to every rank (next block's theta0,
-            // runner.cpp:145-147); residual rows are gathered everywhere.
-            if (final_state) {
-                if (pf->rank == pf->world - 1)
-                    PSWE_CUDA(cudaMemcpyAsync(final_state, st_ptr(pf->fine, pf->mf - 1), state_bytes(pf->Kf),
-                                              cudaMemcpyDeviceToDevice, st));
-                api.check(api.Broadcast(final_state, final_state, state_bytes(pf->Kf) / sizeof(double), ncclFloat64,
-                                        pf->world - 1, pf->world_comm, st),
-                          "ncclBroadcast(final)");
+            // runner.cpp:145-147), step_final (optional) gathers every rank's, residual rows are
+            // gathered everywhere; end_block bounds every wait by the receive timeout
+            std::vector<double> all((size_t)n * (N + 1));
+            try {
+                run_dist(pf, th, st);
+                // tags first: a mismatch must abort the block before the block-end barrier, so
+                // the peers stop (and stop touching this rank's buffers) instead of going on
+                pf->tr->drain(st);
+                check_tags(pf);
+                pf->tr->end_block(st_ptr(pf->fine, pf->mf - 1), reinterpret_cast<double2*>(final_state),
+                                  reinterpret_cast<double2*>(step_final), pf->d_res + (size_t)pf->rank * (N + 1),
+                                  all.data(), st);
+            } catch (const std::exception& e) {
+                pf->broken = true;
+                pf->tr->abort(e.what());
+                throw;
             }
-            api.check(api.AllGather(pf->d_res + (size_t)pf->rank * (N + 1), pf->d_res_all, N + 1, ncclFloat64,
-                                    pf->world_comm, st),
-                      "ncclAllGather(residuals)");
-            if (residuals) {
-                PSWE_CUDA(cudaMemcpyAsync(residuals, pf->d_res_all, sizeof(double) * n * (N + 1), cudaMemcpyDeviceToHost, st));
-                PSWE_CUDA(cudaStreamSynchronize(st));
-            }
+            if (residuals) std::memcpy(residuals, all.data(), sizeof(double) * all.size());
         }
     });
+}
+
+int pswe_pfasst_run_block(pswe_pfasst* pf, const double* theta0, double* final_state, double* residuals,
+                          void* stream) {
+    return pswe_pfasst_run_block_steps(pf, theta0, nullptr, final_state, residuals, stream);
 }
 
 int pswe_pfasst_messages(const pswe_pfasst* pf, int* out, int max_records) {

@@ -190,7 +190,7 @@ public:
         return reinterpret_cast<const double2*>(arena_ + off_[level] + slot * mb_[level]);
     }
 
-    void end_block(const double2* my_final, double2* final_state, double2* step_finals, const double* res_mine,
+    void end_block(const double2* my_final, double2* final_state, double2* step_finals, const double* d_res_mine,
                    double* res_all, cudaStream_t st) override {
         ++block_;
         const size_t fb = (size_t)3 * c_.Kfinal * sizeof(double2);
@@ -201,8 +201,11 @@ public:
         if (final_state) copy_final_from(last, final_state, st);
         if (step_finals)
             for (int r = 0; r < c_.world; ++r) copy_final_from(r, step_finals + (size_t)r * 3 * c_.Kfinal, st);
-        drain(st);
-        if (res_mine) std::memcpy(seg_->rank[c_.rank].res, res_mine, sizeof(double) * c_.n_res);
+        drain(st);  // bounded wait; the residual copy below then finds the stream idle
+        if (d_res_mine)
+            PSWE_CUDA(cudaMemcpyAsync(seg_->rank[c_.rank].res, d_res_mine, sizeof(double) * c_.n_res,
+                                      cudaMemcpyDeviceToHost, st));
+        PSWE_CUDA(cudaStreamSynchronize(st));
         barrier();  // everyone has read every final and published its residuals
         if (res_all)
             for (int r = 0; r < c_.world; ++r) std::memcpy(res_all + (size_t)r * c_.n_res, seg_->rank[r].res,
@@ -528,9 +531,8 @@ public:
                     PSWE_CUDA(cudaEventRecord(send_done_[l].back(), send_stream_[l]));
                 }
             }
-            PSWE_CUDA(cudaMalloc(&d_final_, (size_t)3 * c.Kfinal * sizeof(double2)));
-            PSWE_CUDA(cudaMalloc(&d_res_, sizeof(double) * c.n_res));
             PSWE_CUDA(cudaMalloc(&d_res_all_, sizeof(double) * c.n_res * c.world));
+            PSWE_CUDA(cudaMallocHost(&h_res_all_, sizeof(double) * c.n_res * c.world));
             warm_up();
         } catch (...) {
             abort("initialisation failed");
@@ -564,7 +566,7 @@ public:
         return reinterpret_cast<const double2*>(b);
     }
 
-    void end_block(const double2* my_final, double2* final_state, double2* step_finals, const double* res_mine,
+    void end_block(const double2* my_final, double2* final_state, double2* step_finals, const double* d_res_mine,
                    double* res_all, cudaStream_t st) override {
         auto& api = nccl();
         const size_t fdb = (size_t)3 * c_.Kfinal * 2;  // doubles
@@ -582,13 +584,13 @@ public:
         if (step_finals)
             api.check(api.AllGather(my_final, step_finals, fdb, ncclFloat64, world_comm_, st), "ncclAllGather(finals)");
         if (res_all) {
-            PSWE_CUDA(cudaMemcpyAsync(d_res_, res_mine, sizeof(double) * c_.n_res, cudaMemcpyHostToDevice, st));
-            api.check(api.AllGather(d_res_, d_res_all_, c_.n_res, ncclFloat64, world_comm_, st),
+            api.check(api.AllGather(d_res_mine, d_res_all_, c_.n_res, ncclFloat64, world_comm_, st),
                       "ncclAllGather(residuals)");
-            PSWE_CUDA(cudaMemcpyAsync(res_all, d_res_all_, sizeof(double) * c_.n_res * c_.world,
-                                      cudaMemcpyDeviceToHost, st));
+            PSWE_CUDA(cudaMemcpyAsync(h_res_all_, d_res_all_, sizeof(double) * c_.n_res * c_.world,
+                                      cudaMemcpyDeviceToHost, st));  // pinned: stays asynchronous
         }
         drain(st);
+        if (res_all) std::memcpy(res_all, h_res_all_, sizeof(double) * c_.n_res * c_.world);
     }
 
     void drain(cudaStream_t st) override {
@@ -671,11 +673,10 @@ private:
         }
         if (aux_) cudaStreamDestroy(aux_);
         aux_ = nullptr;
-        if (d_final_) cudaFree(d_final_);
-        if (d_res_) cudaFree(d_res_);
         if (d_res_all_) cudaFree(d_res_all_);
-        d_final_ = nullptr;
-        d_res_ = d_res_all_ = nullptr;
+        if (h_res_all_) cudaFreeHost(h_res_all_);
+        h_res_all_ = nullptr;
+        d_res_all_ = nullptr;
     }
 
     TransportConfig c_;
@@ -685,8 +686,8 @@ private:
     cudaStream_t aux_ = nullptr;
     std::vector<char*> send_buf_[3], recv_buf_[3];
     std::vector<cudaEvent_t> send_done_[3], staged_[3];
-    double2* d_final_ = nullptr;
-    double *d_res_ = nullptr, *d_res_all_ = nullptr;
+    double* d_res_all_ = nullptr;
+    double* h_res_all_ = nullptr;
     bool aborted_ = false;
 };
 

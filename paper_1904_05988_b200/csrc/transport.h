@@ -71,9 +71,9 @@ public:
     // end of a block: waits (bounded by the timeout) for st to drain, then
     //   final_state (device, may be NULL) := the last rank's `my_final`,
     //   step_finals (device, may be NULL) := every rank's `my_final` in rank order,
-    //   res_all (host, world * n_res) := every rank's res_mine (host, n_res)
+    //   res_all (host, world * n_res) := every rank's d_res_mine (device, n_res)
     virtual void end_block(const double2* my_final, double2* final_state, double2* step_finals,
-                           const double* res_mine, double* res_all, cudaStream_t st) = 0;
+                           const double* d_res_mine, double* res_all, cudaStream_t st) = 0;
     // wait for st with the deadlock guard (throws "pipeline deadlock suspected" after the timeout)
     virtual void drain(cudaStream_t st) = 0;
     // tell the peers this rank failed (they stop waiting for it)
