@@ -71,25 +71,38 @@ def bench_states(R=R_BENCH, n=BATCH, seed=20261019):
 # reference arm / CPU baseline (oracle/_ref = the reference C++ compiled from its own sources)
 
 
-def reference_eval_rate(seconds: float, threads: int | None = None):
+# the workload both arms print (identical dicts: the driver compares them)
+CONFIG = {"workload": f"rhs_eval T{R_BENCH} {NLAT}x{NLON} x{BATCH} states", "R": R_BENCH, "nlat": NLAT,
+          "nlon": NLON, "batch_states": BATCH}
+
+
+def reference_step_times(steps: int, warmup: int, budget_s: float | None = None):
+    """The reference's eval_nonlinear + eval_linear (oracle/_ref, swe.cpp:9-69) on bench.py's step:
+    the 5 bench_states at T255 256x512, one state after the other, OpenMP on every host core.
+    Returns (per-step wall times, cores). With budget_s the run stops once that much time is spent
+    (at least one timed step) - the cpu_baseline leg's bounded sample; the reference arm times
+    exactly `steps`. Both legs time the same thing the same way."""
     from oracle import ref_lib as ref
     from oracle.pswe_oracle import ModelParams
-    if threads:
-        ref.lib().ref_set_threads(threads)
-    cores = ref.lib().ref_max_threads()
     plan = ref.RefPlan(R_BENCH, NLAT, NLON)
-    st = bench_states(n=1)[0]
+    states = bench_states()
     p = ModelParams(phi_bar=9.80616 * 1e4)
-    ref.lib()  # noqa
-    plan.time_eval(st, p, 1)  # warm
-    n, t0 = 0, time.perf_counter()
-    while True:
-        plan.time_eval(st, p, 1)
-        n += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
+    cores = ref.lib().ref_max_threads()
+
+    def step():
+        for st in states:
+            plan.time_eval(st, p, 1)
+
+    for _ in range(warmup):
+        step()
+    times, t_start = [], time.perf_counter()
+    while len(times) < steps:
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+        if budget_s is not None and time.perf_counter() - t_start >= budget_s:
             break
-    return n / el, cores, f"{n} sequential eval_nonlinear+eval_linear calls at T255 {NLAT}x{NLON} ({el:.1f} s)"
+    return times, cores
 
 
 def reference_pfasst(n_ts: int, theta0=None, config: int = 3):
@@ -123,23 +136,7 @@ def run_reference_arm(args):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpintswe_ref.so not built"}))
         return
-    from oracle.pswe_oracle import ModelParams
-    plan = ref.RefPlan(R_BENCH, NLAT, NLON)
-    states = bench_states()
-    p = ModelParams(phi_bar=9.80616 * 1e4)
-    cores = ref.lib().ref_max_threads()
-
-    def step():
-        for s in states:
-            plan.time_eval(s, p, 1)
-
-    for _ in range(args.warmup):
-        step()
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        step()
-        times.append(time.perf_counter() - t0)
+    times, cores = reference_step_times(args.steps, args.warmup)
     total = sum(times)
     value = BATCH * args.steps / total
     line = {
@@ -147,8 +144,7 @@ def run_reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded balanced n^-3 random states, 40 m/s rms)",
-        "config": {"workload": f"rhs_eval T{R_BENCH} {NLAT}x{NLON} x{BATCH} states", "R": R_BENCH, "nlat": NLAT,
-                   "nlon": NLON, "batch_states": BATCH},
+        "config": dict(CONFIG),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "reference",
                          "sample": f"{args.steps} steps x {BATCH} evals, reference eval_nonlinear+eval_linear "
                                    f"(OpenMP {cores} threads, FFTW-API shim)"},
@@ -479,10 +475,13 @@ def run_ours(args):
     clk = clocks.stop()
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:  # rank 0 only, after every timed region (also at N > 1)
         try:
-            v, cores, sample = reference_eval_rate(10.0)
-            cpu = {"value": v, "unit": "evals/s", "cores": cores, "kind": "reference", "sample": sample}
+            times, cores = reference_step_times(1000, 1, budget_s=10.0 if world == 1 else 5.0)
+            cpu = {"value": BATCH * len(times) / sum(times), "unit": "evals/s", "cores": cores, "kind": "reference",
+                   "sample": f"{len(times)} steps x {BATCH} evals (bench step: T{R_BENCH} {NLAT}x{NLON}, the 5 "
+                             f"bench_states), reference eval_nonlinear+eval_linear, OpenMP {cores} threads, "
+                             f"timed like --impl reference ({sum(times):.1f} s)"}
         except Exception as e:
             cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -493,11 +492,10 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded balanced n^-3 random states, 40 m/s rms; BASELINE config shapes)",
-            "config": {"workload": f"rhs_eval T{R_BENCH} {NLAT}x{NLON} x{BATCH} states per rank per step",
-                       "R": R_BENCH, "nlat": NLAT, "nlon": NLON, "batch_states": BATCH,
-                       "legendre": "recompute" if args.legendre == 0 else "stream",
-                       "l2": "flushed between timed steps (256 MiB write, outside the timed span)",
-                       "parallelism": f"{world} rank(s), independent states per rank"},
+            "config": dict(CONFIG),
+            "run": {"legendre": "recompute" if args.legendre == 0 else "stream",
+                    "l2": "flushed between timed steps (256 MiB write, outside the timed span)",
+                    "parallelism": f"{world} rank(s), {BATCH} independent states per rank per step"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": gpu_launches,
             "transform": transform, "pfasst": pf_res, "sequential_single_state": sequential,
             "dealiased_grid": dealiased, "pfasst_configs": pf_all,
