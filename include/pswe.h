@@ -198,6 +198,16 @@ int pswe_pfasst3_create_serial(pswe_pair* fine_mid, pswe_pair* mid_coarse, const
                                pswe_pfasst** out);
 int pswe_pfasst3_create_nccl(pswe_pair* fine_mid, pswe_pair* mid_coarse, const pswe_block_config* cfg, int rank,
                              int world, const void* nccl_unique_id, pswe_pfasst** out);
+/* Three-level options. node0_form: how a level's node 0 is updated after its IC receive
+ * (pfasst.cpp:171-174 is the two-level rule):
+ *   PSWE_NODE0_LOWMODE   (default) received state with its modes <= R of the next coarser level
+ *                        replaced by that level's node 0;
+ *   PSWE_NODE0_REFERENCE the reference's additive form on every level: received state + the
+ *                        node-0 increment of the coarsest correction (interpolated up).
+ * mid_sweeps: mid-level sweeps per V-cycle leg (default 1; 0..4). */
+#define PSWE_NODE0_LOWMODE 0
+#define PSWE_NODE0_REFERENCE 1
+int pswe_pfasst3_configure(pswe_pfasst* pf, int node0_form, int mid_sweeps);
 int pswe_pfasst_destroy(pswe_pfasst* pf);
 /* Runs one block from theta0 (device, fine state). On return:
  *   final_state (device): fine last-node state of the LAST time step of the block (the

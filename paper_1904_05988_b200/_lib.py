@@ -80,6 +80,7 @@ SIGNATURES = {
     "pswe_transport_unique_id": (_i, [_i, _vp]),
     "pswe_pfasst_create_dist": (_i, [_vp, _vp, ctypes.POINTER(BlockConfig), _i, _i, _i, _vp, ctypes.POINTER(_vp)]),
     "pswe_pfasst_set_recv_timeout": (_i, [_vp, _d]),
+    "pswe_pfasst3_configure": (_i, [_vp, _i, _i]),
     "pswe_pfasst_run_block_steps": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_pfasst_destroy": (_i, [_vp]),
     "pswe_pfasst_run_block": (_i, [_vp, _vp, _vp, _vp, _vp]),

@@ -90,10 +90,10 @@ struct Op {
     int code, phase, iter, arg;  // arg: use_tau for sweeps, residual index, message step char
 };
 
-std::vector<Op> build_schedule3(int w, int n, int n_iter);
+std::vector<Op> build_schedule3(int w, int n, int n_iter, int mid_sweeps);
 
-std::vector<Op> build_schedule(int w, int n, int n_iter, int nlev = 2) {
-    if (nlev == 3) return build_schedule3(w, n, n_iter);
+std::vector<Op> build_schedule(int w, int n, int n_iter, int nlev = 2, int mid_sweeps = 1) {
+    if (nlev == 3) return build_schedule3(w, n, n_iter, mid_sweeps);
     std::vector<Op> ops;
     ops.push_back({OP_PREDICT_INIT, 0, 0, 0});
     for (int q = 0; q <= w; ++q) {
@@ -133,7 +133,9 @@ std::vector<Op> build_schedule(int w, int n, int n_iter, int nlev = 2) {
 // R tau_mid), runs the pipelined coarse sweep, then goes back up: coarse increment -> mid, mid IC
 // from w-1 (low modes from the coarse node 0), mid sweep (up), mid increment -> fine, fine IC from
 // w-1 (low modes from the mid node 0).
-std::vector<Op> build_schedule3(int w, int n, int n_iter) {
+// mid_sweeps: mid-level sweeps on each leg of the V-cycle (1; 0 only for the degenerate-chain
+// check of tests/test_gpu_pfasst3.py, where the mid level equals the fine one)
+std::vector<Op> build_schedule3(int w, int n, int n_iter, int mid_sweeps) {
     std::vector<Op> ops;
     ops.push_back({OP_PREDICT_INIT, 0, 0, 0});
     for (int q = 0; q <= w; ++q) {
@@ -158,7 +160,7 @@ std::vector<Op> build_schedule3(int w, int n, int n_iter) {
         ops.push_back({OP_REFRESH_MID_ALL, 1, k, 0});
         ops.push_back({OP_SAVE, 1, k, 0});
         ops.push_back({OP_FAS_FM, 1, k, 0});
-        ops.push_back({OP_SWEEP_MID, 1, k, 0});
+        for (int i = 0; i < mid_sweeps; ++i) ops.push_back({OP_SWEEP_MID, 1, k, 0});
         if (w < n - 1) ops.push_back({OP_SEND_MID, 1, k, 'M'});
         ops.push_back({OP_RESTRICT_MC, 1, k, 0});
         ops.push_back({OP_REFRESH_COARSE_ALL, 1, k, 0});
@@ -171,7 +173,7 @@ std::vector<Op> build_schedule3(int w, int n, int n_iter) {
         ops.push_back({OP_INTERP_INC_MC, 1, k, 0});
         if (w > 0) ops.push_back({OP_RECV_MID_IC, 1, k, 0});
         ops.push_back({OP_REFRESH_MID0, 1, k, 0});
-        ops.push_back({OP_SWEEP_MID, 1, k, 0});
+        for (int i = 0; i < mid_sweeps; ++i) ops.push_back({OP_SWEEP_MID, 1, k, 0});
         ops.push_back({OP_INTERP_INC, 1, k, 0});
         if (w > 0) ops.push_back({OP_RECV_FINE_IC, 1, k, 0});
         ops.push_back({OP_REFRESH_FINE0, 1, k, 0});
@@ -244,6 +246,10 @@ struct pswe_pfasst {
     // serial emulation replays the whole block as one CUDA graph (captured on the 2nd call,
     // after an eager call has sized every pool); theta0 is copied into d_theta first
     bool use_graph = true;
+    // three levels: node-0 update form (PSWE_NODE0_LOWMODE default / PSWE_NODE0_REFERENCE) and
+    // mid-level sweeps per V-cycle leg (pswe_pfasst3_configure)
+    int node0 = PSWE_NODE0_LOWMODE;
+    int mid_sweeps = 1;
     int eager_runs = 0;
     double2* d_theta = nullptr;
     cudaGraphExec_t graph = nullptr;
@@ -303,7 +309,7 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
     const double dt = pf->cfg.dt;
     pswe_level *F = pf->fine, *C = pf->coarse, *M = pf->mid;
     const int lc = pf->nlev - 1;  // message level of the coarsest level
-    for (const Op& o : build_schedule(w, n, N, pf->nlev)) {
+    for (const Op& o : build_schedule(w, n, N, pf->nlev, pf->mid_sweeps)) {
         switch (o.code) {
             case OP_PREDICT_INIT:
                 pswe_restrict_space(pf->Rf, pf->Rc, reinterpret_cast<const double*>(theta0),
@@ -347,16 +353,25 @@ __global__ void add_state_kernel(double2* dst, const double2* a, const double2* 
     if (i < n) dst[i] = make_double2(a[i].x + b[i].x, a[i].y + b[i].y);
 }
 
-// received IC + the receiver's own interpolated node-0 increment (pfasst.cpp:171-174): the
-// reference's two-level form (fine level only). Three-level chains use low-mode replacement
-// instead (replace_low_modes below).
-bool has_dstate(const pswe_pfasst* pf, int level) { return level == 0 && pf->nlev == 2; }
+// Node-0 update after the IC receive (pfasst.cpp:171-174). Two levels: the received state + the
+// receiver's own interpolated node-0 increment (the reference's form). Three levels:
+//   * PSWE_NODE0_REFERENCE — the same additive form on every level, generalised so that a level
+//     adds only the correction that came from the COARSEST level: mid node 0 := recv + dstate0_mid
+//     (the node-0 part of the coarse increment interpolated into the mid level), fine node 0 :=
+//     recv + interpolate_space(dstate0_mid). With a degenerate chain (mid level = fine level, no
+//     mid sweeps) this is exactly the two-level reference (tests/test_gpu_pfasst3.py);
+//   * PSWE_NODE0_LOWMODE (default) — low-mode replacement, below.
+bool node0_additive(const pswe_pfasst* pf) { return pf->nlev == 2 || pf->node0 == PSWE_NODE0_REFERENCE; }
+bool has_dstate(const pswe_pfasst* pf, int level) { return node0_additive(pf) && level <= pf->nlev - 2; }
+// three-level reference form: the fine IC's increment is the coarse correction's node-0 part,
+// carried up from the mid level
+void prepare_dstate(pswe_pfasst* pf, int level, cudaStream_t st) {
+    if (pf->nlev == 3 && level == 0 && node0_additive(pf))
+        if (pswe_interpolate_space(pf->Rm, pf->Rf, reinterpret_cast<const double*>(pf->d_dstate0_mid),
+                                   reinterpret_cast<double*>(pf->d_dstate0), 1, st) != 0)
+            throw std::runtime_error(pswe_last_error());
+}
 
-// Three-level IC update: node 0 of level l := received state with its coefficients (m, s) <= R_{l+1}
-// replaced by node 0 of level l+1, i.e. recv + pad(c0 - trunc(recv)). The two-level form above
-// measures the coarse increment against the OLD restricted node 0 while the received state is
-// already new, so the low-mode part of the IC change is counted twice; nested over two levels that
-// diverged (tests/test_gpu_pfasst3.py), while this form has the same fixed point without it.
 __global__ void replace_low_kernel(int Rf, int Rc, double2* __restrict__ dst, const double2* __restrict__ src) {
     const int m = blockIdx.y, f = blockIdx.z;
     const int s = m + blockIdx.x * blockDim.x + threadIdx.x;
@@ -372,7 +387,7 @@ void replace_low_modes(pswe_pfasst* pf, int level, double2* dst, cudaStream_t st
     replace_low_kernel<<<grid, 128, 0, st>>>(Rf, Rc, dst, st_ptr(lower, 0));
     PSWE_LAUNCH_CHECK();
 }
-bool has_low_replace(const pswe_pfasst* pf, int level) { return pf->nlev == 3 && level <= 1; }
+bool has_low_replace(const pswe_pfasst* pf, int level) { return !node0_additive(pf) && level <= 1; }
 void add_dstate0(pswe_pfasst* pf, double2* dst, const double2* msg, cudaStream_t st, int level = 0) {
     const long n = 3 * pf->K_of(level);
     add_state_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dst, msg, level ? pf->d_dstate0_mid : pf->d_dstate0,
@@ -406,6 +421,7 @@ void run_serial(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
         q.pop_front();
         if (m.phase != phase || m.iter != iter || m.level != level)
             throw std::logic_error("pfasst: message tag mismatch");
+        prepare_dstate(pf, level, st);
         if (has_dstate(pf, level)) add_dstate0(pf, dst, m.buf, st, level);
         else PSWE_CUDA(cudaMemcpyAsync(dst, m.buf, state_bytes(K), cudaMemcpyDeviceToDevice, st));
         if (has_low_replace(pf, level)) replace_low_modes(pf, level, dst, st);
@@ -442,6 +458,7 @@ void run_dist(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
     auto recv = [&](int, int level, int phase, int iter, double2* dst, long K) {
         const unsigned long long k = pf->rseq[level]++;
         const double2* slot = T.recv(level, k, st);
+        prepare_dstate(pf, level, st);
         // copy into place (+ the receiver's node-0 increment for the two-level fine IC,
         // pfasst.cpp:171-174) and check the trailer (pfasst.cpp:71-76) in one kernel
         consume_message(dst, slot, has_dstate(pf, level) ? (level ? pf->d_dstate0_mid : pf->d_dstate0) : nullptr,
@@ -559,6 +576,23 @@ int pswe_pfasst3_create_nccl(pswe_pair* fine_mid, pswe_pair* mid_coarse, const p
     return guarded([&] {
         if (!mid_coarse) throw std::invalid_argument("pswe_pfasst3: NULL mid-coarse pair");
         create_dist(fine_mid, mid_coarse, cfg, rank, world, PSWE_TRANSPORT_NCCL, uid, out);
+    });
+}
+
+int pswe_pfasst3_configure(pswe_pfasst* pf, int node0_form, int mid_sweeps) {
+    return guarded([&] {
+        if (!pf) throw std::invalid_argument("NULL argument");
+        if (pf->nlev != 3) throw std::invalid_argument("pswe_pfasst3_configure: not a three-level controller");
+        if (node0_form != PSWE_NODE0_LOWMODE && node0_form != PSWE_NODE0_REFERENCE)
+            throw std::invalid_argument("pswe_pfasst3_configure: unknown node-0 form");
+        if (mid_sweeps < 0 || mid_sweeps > 4) throw std::invalid_argument("pswe_pfasst3_configure: mid_sweeps in 0..4");
+        pf->node0 = node0_form;
+        pf->mid_sweeps = mid_sweeps;
+        if (pf->graph) {  // the captured block follows the old schedule
+            PSWE_CUDA(cudaGraphExecDestroy(pf->graph));
+            pf->graph = nullptr;
+            pf->eager_runs = 0;
+        }
     });
 }
 
@@ -717,7 +751,7 @@ int pswe_pfasst_schedule(int w, int n_time_steps, int n_iter, int* out, int max_
 
 int pswe_pfasst_schedule_ml(int n_levels, int w, int n_time_steps, int n_iter, int* out, int max_ops) {
     if (n_levels != 2 && n_levels != 3) return -1;
-    const auto ops = build_schedule(w, n_time_steps, n_iter, n_levels);
+    const auto ops = build_schedule(w, n_time_steps, n_iter, n_levels, 1);
     if (out)
         for (int i = 0; i < (int)ops.size() && i < max_ops; ++i) {
             out[4 * i] = ops[i].code;

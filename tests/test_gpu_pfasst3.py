@@ -121,3 +121,59 @@ def test_pfasst3_rejects_broken_chain(P):
     fine, mid, coarse, p1, p2 = _chain(P)
     with pytest.raises(Exception):
         P.Pfasst(p2, P.BlockConfig(1, DT, 2), pair2=p1)  # (mid, coarse) then (fine, mid)
+
+
+@pytest.mark.parametrize("n_ts,n_blocks", [(1, 1), (2, 2), (4, 1)])
+def test_degenerate_chain_reproduces_two_level_reference(P, golden, n_ts, n_blocks):
+    """Pin of the three-level controller to the reference (multilevel.hpp:29-35):
+    a chain whose mid level IS the fine level (same plan, 5 nodes: identity transfers, tau_mid = 0)
+    with no mid sweeps and the reference's node-0 form (pfasst.cpp:171-174, generalised to the chain)
+    runs the two-level algorithm through every three-level op (mid restriction / FAS / refresh /
+    message / increments). It must reproduce the reference's two-level pf::run_block (golden
+    pf_nts*, T31/T15, 5/3 nodes, dt 60 s, 3 iterations) to 1e-10 with its residual history."""
+    from oracle import fixtures as fx  # noqa: F401
+    prm = P.ModelParams(phi_bar=PHI_BAR)
+    plan31, plan15 = P.TransformPlan(31), P.TransformPlan(15)
+    fine, mid, coarse = P.Level(plan31, prm, 5), P.Level(plan31, prm, 5), P.Level(plan15, prm, 3)
+    pf = P.Pfasst(P.TransferPair(fine, mid), P.BlockConfig(n_ts, 60.0, 3), pair2=P.TransferPair(mid, coarse))
+    pf.configure3("reference", mid_sweeps=0)
+    fin, hist = P.run_blocks(pf, torch.as_tensor(golden["pf_theta0"]).cuda(), n_blocks)
+    fin = host(fin)
+    assert rel_diff_fields(fin, golden[f"pf_nts{n_ts}_final"]) < 1e-10
+    floor = 64 * 2.0**-52 * np.abs(fin[0]).max()
+    ref = golden[f"pf_nts{n_ts}_res"]
+    assert np.all(np.abs(hist - ref) <= 1e-6 * np.abs(ref) + floor), (hist, ref)
+    # the same chain with the low-mode node-0 form is a different (non-reference) iteration
+    pf.configure3("lowmode", mid_sweeps=0)
+    fin2, _ = P.run_blocks(pf, torch.as_tensor(golden["pf_theta0"]).cuda(), n_blocks)
+    if n_ts > 1:
+        assert rel_diff_fields(host(fin2), golden[f"pf_nts{n_ts}_final"]) > 1e-10
+
+
+@pytest.mark.parametrize("n_ts", [1, 4])
+def test_reference_node0_form_fixed_point(P, n_ts):
+    """Why the three-level default is the low-mode form: the reference's additive node-0 rule
+    (pfasst.cpp:171-174) adds the interpolated coarse increment to an IC that is already new, so
+    for n_ts >= 2 its iteration does not settle on the serial fine collocation solution - in the
+    reference's own two-level algorithm (our two-level controller, pinned to pf::run_block above)
+    and in the chain alike. n_ts = 1 (no IC messages) converges with either form."""
+    fine, mid, coarse, p1, p2 = _chain(P)
+    th0 = _theta0(P)
+    th_t = P.interpolate_space(P.restrict_space(th0, 31, 15), 15, 31)
+    sref = P.Level(P.TransformPlan(31), P.ModelParams(phi_bar=PHI_BAR), 5)
+    ref, _ = P.sdc_run(sref, th_t, DT, 40, n_ts)
+    ref = host(ref)
+    n_iter = 12 + 3 * n_ts
+    pf3 = P.Pfasst(p1, P.BlockConfig(n_ts, DT, n_iter), pair2=p2)
+    pf3.configure3("reference", mid_sweeps=1)
+    fin3 = host(pf3.run_block(th0)[0])
+    prm = P.ModelParams(phi_bar=PHI_BAR)
+    two = P.Pfasst(P.TransferPair(P.Level(P.TransformPlan(31), prm, 5), P.Level(P.TransformPlan(15), prm, 3)),
+                   P.BlockConfig(n_ts, DT, n_iter))
+    fin2 = host(two.run_block(th0)[0])
+    for fin in (fin3, fin2):
+        assert np.all(np.isfinite(fin))
+        if n_ts == 1:
+            assert rel_diff_fields(fin, ref) < 1e-10
+        else:
+            assert rel_diff_fields(fin, ref) > 1e-6
