@@ -499,6 +499,231 @@ void fwd_gt_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out,
     PSWE_LAUNCH_CHECK();
 }
 
+// ---- forward, column-warp mapping ---------------------------------------------------------
+// Same tasks (<= 8 chunk slots of <= 2 orders), the same producer warp / mbarrier ring of {G tiles,
+// P tiles} stages and the same epilogue as leg_fwd_gt_kernel, but the work is split by COLUMN
+// TILE instead of by chunk: compute warp w = (column tile w % NTC, slot group w / NTC) computes its
+// 8 columns against every chunk slot of its group. Per k-step a warp forms G_E = G_N + G_S and
+// G_O = G_N - G_S for ONE column tile per order (2 shared loads, 2 additions) and reuses them for
+// 2 DMMA per slot: in leg_fwd_gt_kernel every warp re-formed all NTC tiles (NTC additions per
+// 2 NTC DMMA, 1/8 of the FP64 pipe - the additions share the pipe with DMMA - and 25% of the
+// instructions, profiles/r01_ncu_eval_kernels_r01l.txt). H slot groups: 8 / H chunk slots per
+// warp (H = 1 for wide column groups, more warps for narrow ones).
+#ifndef PSWE_FWD_CW
+#define PSWE_FWD_CW 1
+#endif
+// one ring stage of leg_fwd_gt_cw_kernel: slots 0..NA-1 of this warp belong to the task's first
+// order (G at g0), the others to its second (G at g0 + gstage)
+template <int NTC, int SPW, int SUB, int NA>
+__device__ __forceinline__ void cw_stage(double (&acc)[SPW][2][2], const double* g0, const double* pt, int gstage,
+                                         int gsub, int sgc, int nt, int r4, int c4) {
+    constexpr int PS = SUB * 128;
+#pragma unroll
+    for (int sub = 0; sub < SUB; ++sub) {
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            const int rr = 4 * ks + c4;
+            const int cs = (8 * nt + r4) ^ gt_swz(NTC, rr);
+            double be[SPW], bo[SPW];
+#pragma unroll
+            for (int u = 0; u < SPW; ++u) {
+                be[u] = pt[u * PS + sub * 128 + rr * 16 + pswz(c4, r4)];
+                bo[u] = pt[u * PS + sub * 128 + rr * 16 + pswz(c4, 8 + r4)];
+            }
+            double aea = 0.0, aoa = 0.0, aeb = 0.0, aob = 0.0;
+            if constexpr (NA > 0) {
+                const double* g = g0 + sub * gsub;
+                const double gn = g[rr * sgc + cs], gs = g[(8 + rr) * sgc + cs];
+                aea = gn + gs;
+                aoa = gn - gs;
+            }
+            if constexpr (NA < SPW) {
+                const double* g = g0 + gstage + sub * gsub;
+                const double gn = g[rr * sgc + cs], gs = g[(8 + rr) * sgc + cs];
+                aeb = gn + gs;
+                aob = gn - gs;
+            }
+#pragma unroll
+            for (int u = 0; u < SPW; ++u) {
+                dmma(acc[u][0], u < NA ? aea : aeb, be[u]);
+                dmma(acc[u][1], u < NA ? aoa : aob, bo[u]);
+            }
+        }
+    }
+}
+
+template <int NTC, int H, int S, int SUB>
+__global__ void __launch_bounds__(32 * (NTC * H + 1), (NTC * H + 1) <= 8 ? 2 : 1)
+    leg_fwd_gt_cw_kernel(int R, int Jp, int nq, GtLayout gl, const double* __restrict__ ptab,
+                         const int* __restrict__ cbase, const int4* __restrict__ tasks_a,
+                         const int2* __restrict__ tasks_b, const double* __restrict__ gt,
+                         double2* __restrict__ out, const int* __restrict__ cstart) {
+    constexpr int NS = 8;       // chunk slots per task (task table: W x CPW = 8)
+    constexpr int SPW = NS / H;  // slots per warp
+    constexpr int WC = NTC * H;  // compute warps
+    extern __shared__ __align__(128) double smem[];
+    __shared__ long pbase[NS], pstride[NS];
+    __shared__ int npc, nst_s;
+    const int sgc = gl.sgc;
+    const int gsub = 2 * 8 * sgc;
+    const int gstage = SUB * gsub;
+    constexpr int PS = SUB * 128;
+    double* sG = smem;                // [S][2 orders][SUB][2][8][sgc]
+    double* sP = sG + S * 2 * gstage;  // [S][NS][SUB * 8 * 16]
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(sP + S * NS * PS);
+    unsigned long long* empty = full + S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int4 ta = tasks_a[blockIdx.x];
+    const int2 tb = tasks_b[blockIdx.x];
+    const int na = ta.z, nb = tb.y;
+    const int z = blockIdx.y;
+    const int ns8 = gl.ns8;
+    const double* __restrict__ ga = gt + ((long)z * (R + 1) + ta.x) * ns8 * gsub;
+    const double* __restrict__ gb = gt + ((long)z * (R + 1) + ta.w) * ns8 * gsub;
+    const int r4 = lane >> 2, c4 = lane & 3;
+    const unsigned GB = (unsigned)gstage * sizeof(double);
+    const int nt = warp % NTC, hg = warp / NTC;  // column tile, slot group
+    const int u0 = hg * SPW;                      // first slot of this warp
+
+    if (threadIdx.x == 0) {
+        int n = 0;  // slots: order a's chunks, then order b's
+        for (int i = 0; i < na + nb; ++i) {
+            const bool b = i >= na;
+            const int m = b ? ta.w : ta.x;
+            const int c = b ? tb.x + (i - na) : ta.y + i;
+            const int nchm = (R + 2 - m + CH - 1) / CH;
+            pbase[n] = ptile_off(cbase[m], nchm, Jp >> 5, c, 0);
+            pstride[n] = (long)nchm * 512;
+            ++n;
+        }
+        npc = n;
+        for (int k = 0; k < S; ++k) {
+            mbar_init(full + k, 1);
+            mbar_init(empty + k, WC);
+        }
+        mbar_fence_init();
+    }
+    if (warp == 0) {  // polar skip at block granularity (as leg_fwd_gt_kernel)
+        const int nsl = Jp >> 5;
+        int nsl_eff = nsl;
+        if (cstart) {
+            const int ca = ta.y + na - 1, cb = tb.x + nb - 1;
+            bool sig = false;
+            if (lane < nsl) {
+                sig = ca >= cstart[ta.x * nsl + lane];
+                if (nb > 0) sig = sig || cb >= cstart[ta.w * nsl + lane];
+            }
+            const unsigned bm = __ballot_sync(0xffffffffu, sig);
+            nsl_eff = 32 - __clz((int)bm);
+        }
+        if (lane == 0) nst_s = (nsl_eff * 4) / SUB;
+    }
+    __syncthreads();
+    pdl_trigger();
+    const int np = npc;
+    const int nst = nst_s;
+    auto issue_p = [&](int q) {
+        const int k = q % S;
+        constexpr unsigned PB = PS * sizeof(double);
+        mbar_expect_tx(full + k, GB * (nb > 0 ? 2u : 1u) + np * PB);
+        const int sub0 = q * SUB;
+        for (int u = 0; u < np; ++u)
+            bulk_g2s(sP + (k * NS + u) * PS, ptab + pbase[u] + (sub0 >> 2) * pstride[u] + (sub0 & 3) * 128, PB,
+                     full + k);
+    };
+    auto issue_g = [&](int q) {
+        const int k = q % S;
+        bulk_g2s(sG + (k * 2) * gstage, ga + (long)q * gstage, GB, full + k);
+        if (nb > 0) bulk_g2s(sG + (k * 2 + 1) * gstage, gb + (long)q * gstage, GB, full + k);
+    };
+    if (threadIdx.x == 0)
+        for (int q = 0; q < S && q < nst; ++q) issue_p(q);
+    pdl_wait();  // G tiles come from the grid stage
+    if (threadIdx.x == 0)
+        for (int q = 0; q < S && q < nst; ++q) issue_g(q);
+
+    if (warp == WC) {  // producer warp: ring refills only
+        if (lane == 0)
+            for (int q = 0; q + S < nst; ++q) {
+                mbar_wait(empty + q % S, (unsigned)(q / S) & 1u);
+                issue_p(q + S);
+                issue_g(q + S);
+            }
+        return;
+    }
+    // slots of this warp: u0 .. u0 + SPW - 1; slot u is order a's chunk u (u < na) or order b's
+    const int my_na = max(0, min(SPW, na - u0));           // order-a slots among mine
+    const int my_n = max(0, min(SPW, na + nb - u0));       // live slots among mine
+    double acc[SPW][2][2];
+#pragma unroll
+    for (int u = 0; u < SPW; ++u) acc[u][0][0] = acc[u][0][1] = acc[u][1][0] = acc[u][1][1] = 0.0;
+
+    for (int q = 0; q < nst; ++q) {
+        const int k = q % S;
+        const unsigned ph = (unsigned)(q / S) & 1u;
+        mbar_wait(full + k, ph);
+        __syncwarp();
+        if (my_n > 0) {
+            const double* g0 = sG + (k * 2) * gstage;
+            const double* pt = sP + (k * NS + u0) * PS;
+            // the order split of this warp's slots as a compile-time constant: straight-line code,
+            // every fragment loaded before the k-step's DMMAs (slots past my_n compute on stale
+            // shared memory and are never stored)
+            switch (my_na) {
+#define PSWE_CW_CASE(NA) \
+    case NA: if constexpr (NA <= SPW) cw_stage<NTC, SPW, SUB, NA>(acc, g0, pt, gstage, gsub, sgc, nt, r4, c4); break;
+                PSWE_CW_CASE(0) PSWE_CW_CASE(1) PSWE_CW_CASE(2) PSWE_CW_CASE(3) PSWE_CW_CASE(4)
+                PSWE_CW_CASE(5) PSWE_CW_CASE(6) PSWE_CW_CASE(7) PSWE_CW_CASE(8)
+#undef PSWE_CW_CASE
+                default: break;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + k);
+    }
+    if (my_n == 0) return;
+    const long Kx = (long)(R + 1) * (R + 4) / 2;
+    const int qz = z * 5 * gl.spg;
+    const int col = 8 * nt + r4;
+    const int q = qz + (col >> 1);
+    if ((col >> 1) >= 5 * gl.spg || q >= nq) return;
+#pragma unroll
+    for (int u = 0; u < SPW; ++u) {
+        if (u >= my_n) continue;
+        const int slot = u0 + u;
+        const bool b = slot >= na;
+        const int m = b ? ta.w : ta.x;
+        const int c = b ? tb.x + (slot - na) : ta.y + slot;
+        const long bx = off_ext(R, m);
+        const int len = R + 2 - m;
+#pragma unroll
+        for (int par = 0; par < 2; ++par)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                const int t = c * CH + par + 2 * (2 * c4 + v);
+                if (t >= len) continue;
+                reinterpret_cast<double*>(out + (long)q * Kx + bx + t)[col & 1] = acc[u][par][v];
+            }
+    }
+}
+
+template <int NTC, int H, int S, int SUB>
+void fwd_cw_launch(const pswe_plan& P, const GtLayout& gl, int nq, double2* out, cudaStream_t st) {
+    const int Jp = ((P.J + 31) / 32) * 32;
+    const size_t sm = (size_t)S * SUB * (2 * 2 * 8 * gl.sgc + 8 * 128) * sizeof(double) +
+                      2 * S * sizeof(unsigned long long);
+    auto kern = leg_fwd_gt_cw_kernel<NTC, H, S, SUB>;
+    static int attr = 0;
+    if ((int)sm > attr) {
+        PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        attr = (int)sm;
+    }
+    launch_pdl(kern, dim3(P.n_fwd_tasks, gl.groups), dim3(32 * (NTC * H + 1)), sm, st, P.R, Jp, nq, gl, P.d_ptab2,
+               P.d_chk_off, P.d_fwd_ta, P.d_fwd_tb, P.d_gtile, out,
+               (const int*)(polar_on() ? P.d_cstart : nullptr));
+    PSWE_LAUNCH_CHECK();
+}
+
 // ---- forward, narrow column groups: P fragments straight from the table into registers --------
 // PSWE_FWD_DIRECT (default): for one/two-state batches (NTC <= 3) on grids of up to NSL 32-latitude
 // slices, every warp loads ALL the B fragments of its chunk (NSL x 8 k-steps x {even, odd} - one
@@ -1072,6 +1297,34 @@ void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t s
     static_assert(kFwdCfg[0].warps == 8 && kFwdCfg[0].cpw == 1 && kFwdCfg[0].stages == 4, "cfg 0");
     static_assert(kFwdCfg[1].warps == 4 && kFwdCfg[1].cpw == 2 && kFwdCfg[1].stages == 3, "cfg 1");
     const int nsl = (P.J + 31) / 32;
+    static const int cw_env = [] { const char* e = getenv("PSWE_FWD_CW"); return e ? atoi(e) : PSWE_FWD_CW; }();
+    if (cw_env && gl.ntc >= 4) {
+        // wide column groups (3-5 states): column-warp mapping, 16-latitude stages, 2-deep ring
+        // (measured r02: 5-state batch forward T255 32.8 -> 30.7 us, T511 159.8 -> 145.5 us;
+        // bit-identical to leg_fwd_gt_kernel over tools/eval_dump.py's 80 cases)
+        switch (gl.ntc) {
+            case 4: fwd_cw_launch<4, 2, 2, 2>(P, gl, 5 * n, out, st); break;
+            case 5: fwd_cw_launch<5, 1, 2, 2>(P, gl, 5 * n, out, st); break;
+            default: fwd_cw_launch<7, 1, 2, 2>(P, gl, 5 * n, out, st); break;
+        }
+        return;
+    }
+    // narrow groups (one or two states: the SDC sweeps' chain) on grids beyond the direct kernel's
+    // 64 latitude pairs: column warps in pairs of slot groups (measured, tools/ab_time.py r02: T255
+    // 5-node sweep 135.6 -> 131.7 us with 32-latitude stages; T511 sweep 627 -> 609 us with
+    // 16-latitude stages; at <= 64 pairs the direct kernel stays: T127 coarse sweep 38.0 vs 42.7 us;
+    // four slot groups per column tile (9-warp blocks) measured slower). PSWE_FWD_CW=0 restores
+    // the chunk-per-warp kernel everywhere (A/B).
+    if (cw_env && gl.ntc <= 3 && nsl > 2) {
+        if (P.fwd_cfg == 0) {
+            if (gl.ntc == 2) fwd_cw_launch<2, 2, 2, 4>(P, gl, 5 * n, out, st);
+            else fwd_cw_launch<3, 2, 2, 4>(P, gl, 5 * n, out, st);
+        } else {
+            if (gl.ntc == 2) fwd_cw_launch<2, 2, 2, 2>(P, gl, 5 * n, out, st);
+            else fwd_cw_launch<3, 2, 2, 2>(P, gl, 5 * n, out, st);
+        }
+        return;
+    }
     if (PSWE_FWD_DIRECT && P.fwd_cfg == 0 && gl.ntc <= 3 && nsl <= 2 &&
         (size_t)2 * gl.ns8 * 2 * 8 * gl.sgc * sizeof(double) <= 96 * 1024) {
         // one or two states on grids up to 64 latitude pairs (T127 on 128 x 256: coarse sweep -2%):
