@@ -73,6 +73,7 @@ int pswe_stream_synchronize(void* stream) {
 }
 
 int pswe_synthesise(pswe_plan* P, const double* coeffs, double* grid, int n, void* stream) {
+    PSWE_NVTX("pswe.synthesise");
     return guarded([&] {
         need(P, "plan");
         need(coeffs, "coeffs", n);
@@ -85,6 +86,7 @@ int pswe_synthesise(pswe_plan* P, const double* coeffs, double* grid, int n, voi
 }
 
 int pswe_analyse(pswe_plan* P, const double* grid, double* coeffs, int n, void* stream) {
+    PSWE_NVTX("pswe.analyse");
     return guarded([&] {
         need(P, "plan");
         need(coeffs, "coeffs", n);
@@ -98,6 +100,7 @@ int pswe_analyse(pswe_plan* P, const double* grid, double* coeffs, int n, void* 
 
 int pswe_uv_from_vortdiv(pswe_plan* P, const double* vort, const double* div, double radius, double* u,
                          double* v, int n, void* stream) {
+    PSWE_NVTX("pswe.uv_from_vortdiv");
     return guarded([&] {
         need(P, "plan");
         need(vort, "vort", n);
@@ -115,6 +118,7 @@ int pswe_uv_from_vortdiv(pswe_plan* P, const double* vort, const double* div, do
 
 int pswe_vortdiv_from_uv(pswe_plan* P, const double* u, const double* v, double radius, double* vort,
                          double* div, int n, void* stream) {
+    PSWE_NVTX("pswe.vortdiv_from_uv");
     return guarded([&] {
         need(P, "plan");
         need(vort, "vort", n);
@@ -142,6 +146,7 @@ int pswe_laplacian(int R, const double* x, double radius, double* y, int n, int 
 
 int pswe_eval_explicit(pswe_plan* P, const pswe_params* p, const double* state, double* f_exp, int n,
                        void* stream) {
+    PSWE_NVTX("pswe.eval_explicit");
     return guarded([&] {
         need(P, "plan");
         need(p, "params");
@@ -164,6 +169,7 @@ int pswe_eval_implicit(int R, const pswe_params* p, const double* state, double*
 
 int pswe_eval_imex(pswe_plan* P, const pswe_params* p, const double* state, double* f_imp, double* f_exp, int n,
                    void* stream) {
+    PSWE_NVTX("pswe.eval_imex");
     return guarded([&] {
         need(P, "plan");
         need(p, "params");

@@ -254,7 +254,6 @@ void fft_rows_c2r(const pswe_plan& P, const double2* four, int in_stride, int in
                   bool div_cos, cudaStream_t st) {
     if (n <= 0) return;
     if (fft_rows_ip(P, true, four, nullptr, nullptr, grid, in_stride, in_off, n, div_cos, 0, 1.0, st)) return;
-    if (fft_rows_c2r_t(P, four, in_stride, in_off, grid, n, div_cos, st)) return;
     const size_t sm = 2 * (size_t)P.N * sizeof(double2);
     if (sm > 48 * 1024) PSWE_CUDA(cudaFuncSetAttribute(fft_c2r_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     fft_c2r_kernel<<<dim3(P.nlat, n), 256, sm, st>>>(P.fft, P.R, P.nlat, P.d_fft_tw, P.d_fft_post, four, in_stride,
@@ -267,7 +266,6 @@ void fft_rows_r2c(const pswe_plan& P, const double* grid, double2* four, int out
     if (n <= 0) return;
     if (fft_rows_ip(P, false, nullptr, grid, four, nullptr, out_stride, out_off, n, pre_cos, scale_mode, radius, st))
         return;
-    if (fft_rows_r2c_t(P, grid, four, out_stride, out_off, n, pre_cos, scale_mode, radius, st)) return;
     const size_t sm = 2 * (size_t)P.N * sizeof(double2);
     if (sm > 48 * 1024) PSWE_CUDA(cudaFuncSetAttribute(fft_r2c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     fft_r2c_kernel<<<dim3(P.nlat, n), 256, sm, st>>>(P.fft, P.R, P.nlat, P.d_fft_tw, P.d_fft_post, grid, four,
@@ -280,7 +278,6 @@ void fft_eval_products(const pswe_plan& P, const pswe_params& prm, const double2
                        int n_batch, cudaStream_t st) {
     if (n_batch <= 0) return;
     if (fft_eval_products_ip(P, prm, four_in, four_out, n_batch, st)) return;
-    if (fft_eval_products_t(P, prm, four_in, four_out, n_batch, st)) return;
     int G = 5;
     size_t sm = (size_t)(5 + G) * P.N * sizeof(double2);
     if (sm > 200 * 1024) {

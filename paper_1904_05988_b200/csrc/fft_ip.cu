@@ -1,6 +1,6 @@
 // In-place longitude FFT stage of eval_nonlinear (sm_100a, fp64).
 //
-// Replaces the ping-pong Stockham kernel of fft2.cu for the fused grid stage (swe.cpp:41-54 with
+// Replaces the ping-pong Stockham kernels of fft.cu (kept for lengths without an in-place plan) for the fused grid stage (swe.cpp:41-54 with
 // the FFT halves of uv_from_vortdiv / synthesise / vortdiv_from_uv / analyse, transform.cpp:
 // 101-190). One block per (latitude row, state) holds the 5 complex rows of length N = nlon/2 in
 // shared memory ONCE (no scratch copy):
@@ -38,6 +38,7 @@ constexpr int kIpThreads = 256;
 // 3 blocks/SM: measured single-state eval -1.5 us, transform round trip -4 us, 5-state batch
 // +6 us with plan 1). Other N: plan 1 = plan 0.
 __host__ __device__ constexpr int ip_radix(int N, int s, int pl = 0) {
+    if (N % 8 != 0) return 0;  // every plan ends in a radix-8 pass (N = 25 once matched h = 3)
     if (pl == 1 && N == 256) return s < 2 ? 16 : 0;
     const int h = N / 8;
     int h0 = 0, h1 = 0;
@@ -175,7 +176,7 @@ struct DitGuard {  // passes s, s-1, ..., 0
     }
 };
 
-// Z_k of the half-length c2r trick from X_k and X_{N-k} (fft2.cu c2r_pre_s)
+// Z_k of the half-length c2r trick from X_k and X_{N-k}
 __device__ __forceinline__ double2 c2r_z(double2 a, double2 bb, double2 w) {
     const double2 b = cconj(bb);
     const double2 e = cadd(a, b);

@@ -309,7 +309,13 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
     const double dt = pf->cfg.dt;
     pswe_level *F = pf->fine, *C = pf->coarse, *M = pf->mid;
     const int lc = pf->nlev - 1;  // message level of the coarsest level
+    static const char* const op_name[] = {
+        "", "PREDICT_INIT", "RECV_COARSE_IC", "REFRESH_COARSE0", "SWEEP_COARSE", "SEND_COARSE", "INTERP_STATES",
+        "REFRESH_FINE_ALL", "RESIDUAL", "SWEEP_FINE", "SEND_FINE", "RESTRICT", "REFRESH_COARSE_ALL", "SAVE", "FAS",
+        "INTERP_INC", "RECV_FINE_IC", "REFRESH_FINE0", "INTERP_STATES_MC", "REFRESH_MID_ALL", "RESTRICT_MC",
+        "SAVE_MC", "FAS_MC", "SWEEP_MID", "SEND_MID", "INTERP_INC_MC", "RECV_MID_IC", "REFRESH_MID0", "FAS_FM"};
     for (const Op& o : build_schedule(w, n, N, pf->nlev, pf->mid_sweeps)) {
+        PSWE_NVTX(op_name[o.code]);
         switch (o.code) {
             case OP_PREDICT_INIT:
                 pswe_restrict_space(pf->Rf, pf->Rc, reinterpret_cast<const double*>(theta0),
@@ -633,6 +639,7 @@ int pswe_pfasst_destroy(pswe_pfasst* pf) {
 int pswe_pfasst_run_block_steps(pswe_pfasst* pf, const double* theta0, double* step_final, double* final_state,
                                 double* residuals, void* stream) {
     return guarded([&] {
+        PSWE_NVTX("pswe.pfasst.run_block");
         if (!pf || !theta0) throw std::invalid_argument("NULL argument");
         if (pf->broken) throw std::runtime_error("pfasst: a previous block failed; destroy and recreate the controller");
         const cudaStream_t st = as_stream(stream);

@@ -166,7 +166,7 @@ void pswe_plan::reserve(int batch) {
 static void plan_free(pswe_plan* p) {
     void* ptrs[] = {p->d_mu_n, p->d_seed, p->d_rec, p->d_eps, p->d_rlap, p->d_ptab, p->d_rowc, p->d_roww,
                     p->d_rowmu, p->d_fft_tw, p->d_fft_post, p->d_four_a, p->d_four_b, p->d_proj,
-                    p->d_xcoef, p->d_chk, p->d_chk_off, p->d_fft_roots, p->d_fft_ptw, p->d_fft_iptw, p->d_fft_iptw1, p->d_ptab2, p->d_cstart, p->d_chunk_m, p->d_xtile, p->d_fwd_ta, p->d_fwd_tb, p->d_gtile};
+                    p->d_xcoef, p->d_chk, p->d_chk_off, p->d_fft_roots, p->d_fft_iptw, p->d_fft_iptw1, p->d_ptab2, p->d_cstart, p->d_chunk_m, p->d_xtile, p->d_fwd_ta, p->d_fwd_tb, p->d_gtile};
     for (void* q : ptrs)
         if (q) cudaFree(q);
 }
@@ -290,7 +290,6 @@ static void plan_build(pswe_plan* p, int R, int nlat, int nlon, int mode) {
     p->d_fft_tw = upload(tw);
     p->d_fft_post = upload(post);
     p->d_fft_roots = upload(roots);
-    p->d_fft_ptw = upload(fft_pass_twiddles(p->N));
     p->d_fft_iptw = upload(fft_ip_twiddles(p->N));
     p->d_fft_iptw1 = upload(fft_ip_twiddles(p->N, 1));
 

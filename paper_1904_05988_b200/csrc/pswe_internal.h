@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <stdexcept>
@@ -39,6 +40,18 @@ int guarded(F&& f) {
 }
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// NVTX ranges on the host API (nsys / ncu --nvtx timelines: per ABI call, per PFASST op, per message);
+// header-only NVTX v3, a no-op without an attached tool
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define PSWE_NVTX_CAT2(a, b) a##b
+#define PSWE_NVTX_CAT(a, b) PSWE_NVTX_CAT2(a, b)
+#define PSWE_NVTX(name) ::pswe::NvtxRange PSWE_NVTX_CAT(pswe_nvtx_, __LINE__)(name)
 
 // Programmatic dependent launch (PDL) of the eval chain prep -> inverse -> grid stage -> forward
 // -> tail: each kernel is launched with programmatic stream serialisation, runs its independent
@@ -134,7 +147,6 @@ struct pswe_plan {
     double2* d_fft_tw = nullptr; // stage twiddles
     double2* d_fft_post = nullptr;  // [N+1] exp(-2 pi i k / nlon)
     double2* d_fft_roots = nullptr; // [N] exp(-2 pi i k / N)
-    double2* d_fft_ptw = nullptr;   // per-pass twiddles of the compile-time Stockham (fft2.cu)
     double2* d_fft_iptw = nullptr;  // per-pass twiddles of the in-place DIF/DIT plan (fft_ip.cu)
     double2* d_fft_iptw1 = nullptr; // the same for plan 1 (narrow evaluations, plain row transforms)
     pswe::FftDesc fft{};
@@ -232,8 +244,6 @@ void fft_rows_r2c(const pswe_plan& P, const double* grid, double2* four, int out
 void fft_eval_products(const pswe_plan& P, const pswe_params& prm, const double2* four_in,
                        double2* four_out, int n_batch, cudaStream_t st);
 
-// fft2.cu: compile-time-sized variants; return false if nlon/2 is not instantiated
-std::vector<double2> fft_pass_twiddles(int N);
 // G-tile path of the eval grid stage (STREAM mode): fft_ip.cu writes P.d_gtile, the forward
 // reads it (legendre_stream.cu). gt_path_ok: every precondition of the pair holds for n states.
 bool gt_path_ok(const pswe_plan& P, int n);
@@ -243,16 +253,10 @@ void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t s
 std::vector<double2> fft_ip_twiddles(int N, int pl = 0);
 bool fft_eval_products_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
                           cudaStream_t st);
-bool fft_eval_products_t(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
-                         cudaStream_t st);
 // in-place plain row transforms (fft_ip.cu); false when nlon/2 has no in-place plan
 bool fft_rows_ip(const pswe_plan& P, bool c2r, const double2* four_in, const double* grid_in, double2* four_out,
                  double* grid_out, int stride, int off, int n, bool cos_flag, int scale_mode, double radius,
                  cudaStream_t st);
-bool fft_rows_c2r_t(const pswe_plan& P, const double2* four, int in_stride, int in_off, double* grid, int n,
-                    bool div_cos, cudaStream_t st);
-bool fft_rows_r2c_t(const pswe_plan& P, const double* grid, double2* four, int out_stride, int out_off, int n,
-                    bool pre_cos, int scale_mode, double radius, cudaStream_t st);
 
 // ops.cu
 void eval_tail(const pswe_plan& P, const pswe_params& prm, const double2* proj, const double2* state,

@@ -846,6 +846,7 @@ int pswe_level_info(const pswe_level* L, int* R, int* nn) {
 }
 
 int pswe_spread(pswe_level* L, const double* theta0, void* stream) {
+    PSWE_NVTX("pswe.spread");
     return guarded([&] {
         if (!L || !theta0) throw std::invalid_argument("pswe_spread: NULL argument");
         level_spread(L, reinterpret_cast<const double2*>(theta0), as_stream(stream));
@@ -853,6 +854,7 @@ int pswe_spread(pswe_level* L, const double* theta0, void* stream) {
 }
 
 int pswe_refresh_nodes(pswe_level* L, int first, int count, void* stream) {
+    PSWE_NVTX("pswe.refresh_nodes");
     return guarded([&] {
         if (!L) throw std::invalid_argument("NULL level");
         if (first < 0 || count < 0 || first + count > L->nn) throw std::invalid_argument("refresh: node range");
@@ -861,6 +863,7 @@ int pswe_refresh_nodes(pswe_level* L, int first, int count, void* stream) {
 }
 
 int pswe_sweep(pswe_level* L, double dt, const double* tau, void* stream) {
+    PSWE_NVTX("pswe.sweep");
     return guarded([&] {
         if (!L) throw std::invalid_argument("NULL level");
         level_sweep(L, dt, reinterpret_cast<const double2*>(tau), as_stream(stream));
@@ -868,6 +871,7 @@ int pswe_sweep(pswe_level* L, double dt, const double* tau, void* stream) {
 }
 
 int pswe_collocation_residual(pswe_level* L, double dt, double* out, void* stream) {
+    PSWE_NVTX("pswe.collocation_residual");
     return guarded([&] {
         if (!L || !out) throw std::invalid_argument("NULL argument");
         level_residual(L, dt, out, as_stream(stream));
@@ -875,6 +879,7 @@ int pswe_collocation_residual(pswe_level* L, double dt, double* out, void* strea
 }
 
 int pswe_sdc_step(pswe_level* L, const double* theta0, double dt, int n_sweeps, double* out_res, void* stream) {
+    PSWE_NVTX("pswe.sdc_step");
     return guarded([&] {
         if (!L || !theta0) throw std::invalid_argument("NULL argument");
         const cudaStream_t st = as_stream(stream);

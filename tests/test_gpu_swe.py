@@ -64,9 +64,11 @@ def test_eval_vs_numpy_oracle(P, R, grid):
 def test_large_grid_eval_vs_reference(P, R, grid):
     """T511 on BASELINE config 4's 512x1024 grid: the large-grid forward configuration (4-warp
     tasks, 2 chunks per warp, cut by polar-skip weight) and the single-state one, both against the
-    REFERENCE (oracle/_ref) at 1e-11 per field - the batch-vs-single test alone would not see a chunk
-    the shared task table dropped. (Round 1 compared with the numpy restatement at 1e-10: that
-    restatement itself sits 1.3e-11 from the reference here, tests/test_oracle_golden.py.)"""
+    REFERENCE (oracle/_ref) - the batch-vs-single test alone would not see a chunk the shared task
+    table dropped. Tolerance 2e-11 per field = the two implementations' distances from the EXACT
+    operator added: the GPU is held to 1e-11 of it (tests/test_gpu_precision.py), and the
+    reference build itself sits up to 8.6e-12 from it on these states (seed 11: Phi 5.6e-12,
+    delta 8.6e-12; seed 7: 2.8e-12; oracle/precise.py, long double)."""
     from oracle import ref_lib as ref
     if not ref.available():
         pytest.skip("oracle/_ref not built")
@@ -84,8 +86,8 @@ def test_large_grid_eval_vs_reference(P, R, grid):
     batch = host(P.imex_split(cuda(sts), p, plan)[1])
     for i in (0, 4):
         want = rp.eval_nonlinear(sts[i], p)
-        assert rel_diff_fields(batch[i], want) < 1e-11
-        assert rel_diff_fields(host(P.eval_nonlinear(cuda(sts[i]), p, plan)), want) < 1e-11
+        assert rel_diff_fields(batch[i], want) < 2e-11
+        assert rel_diff_fields(host(P.eval_nonlinear(cuda(sts[i]), p, plan)), want) < 2e-11
 
 
 def test_batched_equals_single(P):
