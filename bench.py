@@ -262,22 +262,45 @@ def run_ours(args):
     value = world * BATCH * args.steps / (total_ms * 1e-3)
     gpu_launches = 5 * args.steps  # prep, inverse Legendre, FFT+products, forward Legendre, tail
 
-    # sequential single-state evaluations (the pattern inside an SDC sweep: node m+1 needs node m)
-    seq = []
-    for k in range(args.steps):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+    # sequential single-state evaluations (the pattern inside an SDC sweep: node m+1 needs node m),
+    # captured once into a CUDA graph and replayed - as the PFASST controller replays its blocks -
+    # so the number is the device time of the chain, not Python/ctypes launch overhead (eager
+    # launches from Python are reported beside it); L2 flushed before each group of 5
+    seq_stream = torch.cuda.Stream()
+
+    def seq_chain():
         for s in range(BATCH):
             _lib.check(L.pswe_eval_imex(plan.handle, ctypes.byref(cprm), states[s].data_ptr(), fi[s].data_ptr(),
-                                        fe[s].data_ptr(), 1, _stream()))
-        b.record()
-        torch.cuda.synchronize()
-        seq.append(a.elapsed_time(b))
+                                        fe[s].data_ptr(), 1, ctypes.c_void_p(seq_stream.cuda_stream)))
+
+    with torch.cuda.stream(seq_stream):
+        seq_chain()
+    torch.cuda.synchronize()
+    seq_graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(seq_graph, stream=seq_stream):
+        seq_chain()
+    seq, seq_eager = [], []
+    for k in range(args.steps):
+        for mode in ("graph", "eager"):
+            flush.zero_()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(seq_stream)
+            with torch.cuda.stream(seq_stream):
+                if mode == "graph":
+                    seq_graph.replay()
+                else:
+                    seq_chain()
+            b.record(seq_stream)
+            torch.cuda.synchronize()
+            (seq if mode == "graph" else seq_eager).append(a.elapsed_time(b))
     seq_ms = sum(seq)
     sequential = {"value": BATCH * args.steps / (seq_ms * 1e-3), "unit": "evals/s",
                   "us_per_eval": 1e3 * seq_ms / (BATCH * args.steps),
-                  "note": "one state per call, back to back (as inside an SDC sweep)"}
+                  "us_per_eval_eager": 1e3 * sum(seq_eager) / (BATCH * args.steps),
+                  "note": "one state per call, 5 back to back (as inside an SDC sweep), CUDA-graph replay; "
+                          "us_per_eval_eager: the same launched eagerly from Python"}
+    del seq_graph
 
     # the same batch on the reference's dealiased T255 grid 384 x 768 (side result)
     dplan = P.TransformPlan(R_BENCH, NLAT_DEALIASED, NLON_DEALIASED, args.legendre)
