@@ -76,6 +76,16 @@ CONFIG = {"workload": f"rhs_eval T{R_BENCH} {NLAT}x{NLON} x{BATCH} states", "R":
           "nlon": NLON, "batch_states": BATCH}
 
 
+def use_all_host_cores(ref):
+    """The reference's OpenMP team on every core this process may run on (torchrun exports
+    OMP_NUM_THREADS=1 to its workers; the reference arm must use all host threads it can)."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    ref.lib().ref_set_threads(n)
+
+
 def reference_step_times(steps: int, warmup: int, budget_s: float | None = None):
     """The reference's eval_nonlinear + eval_linear (oracle/_ref, swe.cpp:9-69) on bench.py's step:
     the 5 bench_states at T255 256x512, one state after the other, OpenMP on every host core.
@@ -84,6 +94,7 @@ def reference_step_times(steps: int, warmup: int, budget_s: float | None = None)
     exactly `steps`. Both legs time the same thing the same way."""
     from oracle import ref_lib as ref
     from oracle.pswe_oracle import ModelParams
+    use_all_host_cores(ref)
     plan = ref.RefPlan(R_BENCH, NLAT, NLON)
     states = bench_states()
     p = ModelParams(phi_bar=9.80616 * 1e4)
@@ -119,6 +130,7 @@ def reference_pfasst(n_ts: int, theta0=None, config: int = 3):
     (Rf, nf_lat, nf_lon, nn_f), (Rc, nc_lat, nc_lon, nn_c) = lv
     th = config_state(config) if theta0 is None else theta0
     p = ModelParams(phi_bar=9.80616 * 1e4)
+    use_all_host_cores(ref)
     r = ref.pfasst_run(Rf, (nf_lat, nf_lon), Rc, (nc_lat, nc_lon), p, nn_f, nn_c, n_ts, dt, n_iter, 1, th,
                        serial=(n_ts == 1))
     cores = ref.lib().ref_max_threads()
@@ -207,6 +219,14 @@ class Clocks:
 # our arm
 
 
+def max_over_ranks(v: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if dist.get_backend() == "gloo" else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args):
     import ctypes
 
@@ -218,9 +238,18 @@ def run_ours(args):
     from paper_1904_05988_b200.transform import _stream
 
     rank, world, local = dist_env()
+    # PSWE_BENCH_SHARED_GPU=1: every rank on cuda:0 with a gloo process group - a functional dry run
+    # of the N > 1 code path (transport set-up, PFASST ranks, max-over-ranks) on a one-GPU box; its
+    # timings are not scaling numbers (the ranks share one GPU)
+    shared = os.environ.get("PSWE_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     L = _lib.lib()
 
@@ -254,9 +283,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     total_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms, dev)
         dist.barrier()
     torch.cuda.synchronize()
     value = world * BATCH * args.steps / (total_ms * 1e-3)
@@ -431,9 +458,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(e2e_ms, dev)
     st_bytes = BATCH * 3 * P.num_coeffs(R_BENCH) * 16
     e2e = {"value": world * BATCH * args.steps / (e2e_ms * 1e-3), "unit": "evals/s",
            "h2d_bytes_per_step": st_bytes, "d2h_bytes_per_step": 2 * st_bytes,
@@ -516,7 +541,7 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded balanced n^-3 random states, 40 m/s rms; BASELINE config shapes)",
             "config": dict(CONFIG),
-            "run": {"legendre": "recompute" if args.legendre == 0 else "stream",
+            "run": {"shared_gpu_dry_run": shared,"legendre": "recompute" if args.legendre == 0 else "stream",
                     "l2": "flushed between timed steps (256 MiB write, outside the timed span)",
                     "parallelism": f"{world} rank(s), {BATCH} independent states per rank per step"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": gpu_launches,
@@ -575,9 +600,7 @@ def run_pfasst(P, prm, world, rank, dev, clocks_dev=0, config=3):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
     wall = ms * 1e-3
     desc = "/".join(f"T{R}({nlat}x{nlon})" for R, nlat, nlon, _ in lv)
     nodes = "/".join(str(nn) for *_, nn in lv)
