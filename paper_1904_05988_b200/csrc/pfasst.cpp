@@ -240,6 +240,11 @@ struct pswe_pfasst {
     double recv_timeout = 300.0;  // BlockConfig::recv_timeout_seconds (pfasst.hpp:19)
     int fault = 0;                // fault injection for tests (PSWE_PFASST_FAULT): 1 = skew tags
     bool broken = false;          // a block failed: the transport state is undefined
+    // distributed: segment graphs (captured on the second block, replayed after; invalidated like
+    // the serial graph when a plan's scratch is reallocated)
+    std::vector<cudaGraphExec_t> seg_graphs;
+    int dist_runs = 0;
+    unsigned long long seg_gen = 0;
     // BlockResult.step_final (pfasst.hpp:34-36): serial: every worker's last fine node [n][3Kf]
     double2* d_step_final = nullptr;
     long K_of(int level) const { return level == 0 ? Kf : (level == nlev - 1 ? Kc : Km); }
@@ -303,8 +308,63 @@ void init_common(pswe_pfasst* pf, pswe_pair* pair, const pswe_block_config* cfg,
 double2* st_ptr(pswe_level* L, int node) { return reinterpret_cast<double2*>(pswe_level_ptr(L, 0, node)); }
 
 // execute the schedule of worker w; send/recv through the callbacks
+bool is_comm(int code) {
+    return code == OP_SEND_COARSE || code == OP_SEND_FINE || code == OP_SEND_MID || code == OP_RECV_COARSE_IC ||
+           code == OP_RECV_FINE_IC || code == OP_RECV_MID_IC;
+}
+
+// Segment graphs of the distributed executor: the ops between two messages (sends and receives
+// stay eager - they touch host-side counters, events and the transport's rings) are captured once
+// per run of compute ops and replayed as one graph launch each.
+struct SegCtl {
+    enum Mode { EAGER, CAPTURE, REPLAY } mode = EAGER;
+    std::vector<cudaGraphExec_t>* graphs = nullptr;
+    size_t next = 0;
+    bool capturing = false;
+    cudaStream_t st = nullptr;
+    void close() {  // end the open capture, instantiate, launch
+        if (!capturing) return;
+        cudaGraph_t g = nullptr;
+        PSWE_CUDA(cudaStreamEndCapture(st, &g));
+        cudaGraphExec_t e = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&e, g, 0);
+        cudaGraphDestroy(g);
+        PSWE_CUDA(ie);
+        graphs->push_back(e);
+        capturing = false;
+        PSWE_CUDA(cudaGraphLaunch(e, st));
+    }
+    // returns true if the compute op must be issued now (eager or being captured)
+    bool compute(bool first_of_run) {
+        if (mode == EAGER) return true;
+        if (mode == CAPTURE) {
+            if (!capturing) {
+                PSWE_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+                capturing = true;
+            }
+            return true;
+        }
+        if (first_of_run) {
+            if (next >= graphs->size()) throw std::logic_error("pfasst: segment graph missing");
+            PSWE_CUDA(cudaGraphLaunch((*graphs)[next++], st));
+        }
+        return false;
+    }
+    void comm() {
+        if (mode == CAPTURE) close();
+    }
+    void abort_capture() {
+        if (!capturing) return;
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        capturing = false;
+    }
+};
+
 template <class SendF, class RecvF>
-void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, SendF&& send, RecvF&& recv) {
+void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, SendF&& send, RecvF&& recv,
+                SegCtl* seg = nullptr) {
     const int n = pf->cfg.n_time_steps, N = pf->cfg.n_iter;
     const double dt = pf->cfg.dt;
     pswe_level *F = pf->fine, *C = pf->coarse, *M = pf->mid;
@@ -314,8 +374,17 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
         "REFRESH_FINE_ALL", "RESIDUAL", "SWEEP_FINE", "SEND_FINE", "RESTRICT", "REFRESH_COARSE_ALL", "SAVE", "FAS",
         "INTERP_INC", "RECV_FINE_IC", "REFRESH_FINE0", "INTERP_STATES_MC", "REFRESH_MID_ALL", "RESTRICT_MC",
         "SAVE_MC", "FAS_MC", "SWEEP_MID", "SEND_MID", "INTERP_INC_MC", "RECV_MID_IC", "REFRESH_MID0", "FAS_FM"};
-    for (const Op& o : build_schedule(w, n, N, pf->nlev, pf->mid_sweeps)) {
+    const std::vector<Op> ops = build_schedule(w, n, N, pf->nlev, pf->mid_sweeps);
+    for (size_t i = 0; i < ops.size(); ++i) {
+        const Op& o = ops[i];
         PSWE_NVTX(op_name[o.code]);
+        if (seg) {
+            if (is_comm(o.code)) {
+                seg->comm();
+            } else if (!seg->compute(i == 0 || is_comm(ops[i - 1].code))) {
+                continue;  // replayed inside this run's segment graph
+            }
+        }
         switch (o.code) {
             case OP_PREDICT_INIT:
                 pswe_restrict_space(pf->Rf, pf->Rc, reinterpret_cast<const double*>(theta0),
@@ -352,6 +421,7 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
             default: throw std::logic_error("pfasst: unknown op");
         }
     }
+    if (seg) seg->close();
 }
 
 __global__ void add_state_kernel(double2* dst, const double2* a, const double2* b, long n) {
@@ -441,7 +511,7 @@ void run_serial(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
     }
 }
 
-void run_dist(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
+void run_dist(pswe_pfasst* pf, const double2* theta0, cudaStream_t st, SegCtl* seg = nullptr) {
     Transport& T = *pf->tr;
     const int w = pf->rank;
     auto tag_of = [&](int level, int phase, int iter, int sender, unsigned long long seq) {
@@ -471,7 +541,12 @@ void run_dist(pswe_pfasst* pf, const double2* theta0, cudaStream_t st) {
                         3 * K, tag_of(level, phase, iter, w - 1, k), pf->d_err, st);
         if (has_low_replace(pf, level)) replace_low_modes(pf, level, dst, st);
     };
-    run_worker(pf, w, theta0, st, send, recv);
+    try {
+        run_worker(pf, w, theta0, st, send, recv, seg);
+    } catch (...) {
+        if (seg) seg->abort_capture();
+        throw;
+    }
 }
 
 void check_tags(pswe_pfasst* pf) {
@@ -616,6 +691,7 @@ int pswe_pfasst_destroy(pswe_pfasst* pf) {
         if (!pf) return;
         cudaDeviceSynchronize();
         if (pf->graph) cudaGraphExecDestroy(pf->graph);
+        for (auto e : pf->seg_graphs) cudaGraphExecDestroy(e);
         if (pf->d_theta) cudaFree(pf->d_theta);
         if (pf->gstream) cudaStreamDestroy(pf->gstream);
         if (pf->ev_in) cudaEventDestroy(pf->ev_in);
@@ -714,7 +790,37 @@ int pswe_pfasst_run_block_steps(pswe_pfasst* pf, const double* theta0, double* s
             // gathered everywhere; end_block bounds every wait by the receive timeout
             std::vector<double> all((size_t)n * (N + 1));
             try {
-                run_dist(pf, th, st);
+                if (pf->use_graph) {
+                    // segment graphs on an internal stream (the caller's may be the legacy stream),
+                    // ordered after / before the caller's stream; theta0 copied to a fixed buffer
+                    if (!pf->d_theta) {
+                        PSWE_CUDA(cudaMalloc(&pf->d_theta, state_bytes(pf->Kf)));
+                        PSWE_CUDA(cudaStreamCreateWithFlags(&pf->gstream, cudaStreamNonBlocking));
+                        PSWE_CUDA(cudaEventCreateWithFlags(&pf->ev_in, cudaEventDisableTiming));
+                        PSWE_CUDA(cudaEventCreateWithFlags(&pf->ev_out, cudaEventDisableTiming));
+                    }
+                    const unsigned long long gen = plans_generation(pf);
+                    if (!pf->seg_graphs.empty() && gen != pf->seg_gen) {
+                        for (auto e : pf->seg_graphs) cudaGraphExecDestroy(e);
+                        pf->seg_graphs.clear();
+                        pf->dist_runs = 0;
+                    }
+                    PSWE_CUDA(cudaMemcpyAsync(pf->d_theta, th, state_bytes(pf->Kf), cudaMemcpyDeviceToDevice, st));
+                    PSWE_CUDA(cudaEventRecord(pf->ev_in, st));
+                    PSWE_CUDA(cudaStreamWaitEvent(pf->gstream, pf->ev_in, 0));
+                    SegCtl seg;
+                    seg.graphs = &pf->seg_graphs;
+                    seg.st = pf->gstream;
+                    seg.mode = !pf->seg_graphs.empty() ? SegCtl::REPLAY
+                                                       : (pf->dist_runs >= 1 ? SegCtl::CAPTURE : SegCtl::EAGER);
+                    run_dist(pf, pf->d_theta, pf->gstream, &seg);
+                    if (seg.mode == SegCtl::CAPTURE) pf->seg_gen = plans_generation(pf);
+                    ++pf->dist_runs;
+                    PSWE_CUDA(cudaEventRecord(pf->ev_out, pf->gstream));
+                    PSWE_CUDA(cudaStreamWaitEvent(st, pf->ev_out, 0));
+                } else {
+                    run_dist(pf, th, st);
+                }
                 // tags first: a mismatch must abort the block before the block-end barrier, so
                 // the peers stop (and stop touching this rank's buffers) instead of going on
                 pf->tr->drain(st);

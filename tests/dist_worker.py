@@ -2,8 +2,9 @@
 module). All ranks may share one GPU with the IPC transport.
 
 python tests/dist_worker.py RANK WORLD TRANSPORT UID_HEX OUT.npz LEVELS MODE TIMEOUT
-  LEVELS 2: T31/T15 (5/3 nodes), the golden pf_nts2 case (2 blocks, dt 60 s, 3 iterations);
-  LEVELS 3: T31/T21/T15 (5/3/2 nodes), 2 blocks;
+  LEVELS 2: T31/T15 (5/3 nodes), the golden pf_nts2 case (dt 60 s, 3 iterations), 3 blocks (the
+            first two are the golden case; eager, segment-graph capture, replay);
+  LEVELS 3: T31/T21/T15 (5/3/2 nodes), 3 blocks;
   MODE normal | hang (this rank never runs a block) | skew (this rank's first iteration message
   carries the wrong iteration tag, PSWE_PFASST_FAULT=1).
 Writes final / residual history / step finals, or the error text."""
@@ -51,12 +52,16 @@ def main():
         s = th.clone()
         hist, steps = [], []
         t0 = time.time()
-        for _ in range(2):
+        final2 = None
+        for b in range(3):  # eager block, segment-graph capture block, replay block
             fin, res, st = pf.run_block(s, step_finals=True)
             s.copy_(fin)
             hist.append(res)
             steps.append(st.cpu().numpy())
-        np.savez(out, final=s.cpu().numpy(), res=np.array(hist), steps=np.array(steps), wall=time.time() - t0,
+            if b == 1:
+                final2 = s.cpu().numpy()
+        np.savez(out, final=s.cpu().numpy(), final2=final2, res=np.array(hist), steps=np.array(steps),
+                 wall=time.time() - t0,
                  messages=np.array([[m[0], m[1], ord(m[2]), m[3], m[4], m[5], m[6]] for m in pf.messages()]))
         pf.close()
     except Exception as e:  # reported to the parent test

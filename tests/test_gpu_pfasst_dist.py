@@ -2,9 +2,9 @@
 transport; the receiver waits on the host, so no GPU work of one process ever waits on the
 other's). This runs the exact ring-slot, tag, event and shared-memory code of the multi-GPU path:
 
-* two-level T31/T15, 2 blocks of n_ts = 2: final state, residual history per iteration and
-  message log equal the reference's (golden pf_nts2_*, oracle/_ref pf::run_block) and are
-  BIT-identical to the serial emulation of the same block; BlockResult.step_final on every rank;
+* two-level T31/T15, 3 blocks of n_ts = 2 (eager, segment-graph capture, graph replay): blocks 1-2
+  equal the reference's (golden pf_nts2_*, oracle/_ref pf::run_block), and every block's final
+  state, residual history, step finals and message log are BIT-identical to the serial emulation;
 * three-level T31/T21/T15: bit-identical to the serial-emulation three-level run;
 * a hung peer makes the other rank fail with the reference's "pipeline deadlock suspected"
   (pfasst.cpp:39-47) within the receive timeout;
@@ -64,7 +64,7 @@ def serial(levels):
         th = torch.as_tensor(balanced_random_state(31, 20.0, 4, phi_bar=prm.phi_bar)).cuda()
     pf = P.Pfasst(pair, P.BlockConfig(2, 60.0, 3), pair2=pair2)
     s, hist, steps = th.clone(), [], []
-    for _ in range(2):
+    for _ in range(3):
         fin, res, st = pf.run_block(s, step_finals=True)
         s.copy_(fin)
         hist.append(res)
@@ -86,9 +86,9 @@ def test_world2_ipc_matches_serial_and_reference(tmp_path, golden, levels):
         np.testing.assert_array_equal(r["steps"], steps_s)
         assert sorted(tuple(int(v) for v in m) for m in r["messages"]) == \
             sorted((m[0], m[1], ord(m[2]), m[3], m[4], m[5], m[6]) for m in msgs_s)
-    if levels == 2:
-        assert rel_diff_fields(res[0]["final"], golden["pf_nts2_final"]) < 1e-10
-        assert res_ok(res[0]["res"], golden["pf_nts2_res"], res[0]["final"])
+    if levels == 2:  # blocks 1-2 are the reference's golden two-block run
+        assert rel_diff_fields(res[0]["final2"], golden["pf_nts2_final"]) < 1e-10
+        assert res_ok(res[0]["res"][:2], golden["pf_nts2_res"], res[0]["final2"])
         ref_log = sorted(tuple(int(v) for v in m) for m in golden["pf_nts2_msgs"])
         assert sorted(tuple(int(v) for v in m) for m in res[1]["messages"]) == ref_log
 
