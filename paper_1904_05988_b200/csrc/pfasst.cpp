@@ -255,6 +255,13 @@ struct pswe_pfasst {
     // mid-level sweeps per V-cycle leg (pswe_pfasst3_configure)
     int node0 = PSWE_NODE0_LOWMODE;
     int mid_sweeps = 1;
+    // Worker 0 receives nothing, so in every iteration its node-0 states stay exactly what they
+    // were (the interpolated coarse increment at node 0 is exactly zero: coarse node 0 is never
+    // changed by a sweep or a receive); the reference still re-evaluates F there after Step C/D
+    // (refresh_node(coarse, 0), pfasst.cpp:152; refresh_node(fine, 0), :175) and gets the same
+    // bits. The executor skips those evaluations for worker 0 (the schedule and the message log
+    // are unchanged); tests/test_gpu_sdc_pfasst.py checks bit-identity with PSWE_PFASST_NO_ELIDE=1.
+    bool elide_w0 = true;
     int eager_runs = 0;
     double2* d_theta = nullptr;
     cudaGraphExec_t graph = nullptr;
@@ -392,7 +399,9 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
                 level_spread(C, st_ptr(C, 0), st);
                 break;
             case OP_RECV_COARSE_IC: recv(w, lc, o.phase, o.iter, st_ptr(C, 0), pf->Kc); break;
-            case OP_REFRESH_COARSE0: level_refresh(C, 0, 1, st); break;
+            case OP_REFRESH_COARSE0:
+                if (!(pf->elide_w0 && w == 0 && o.phase == 1)) level_refresh(C, 0, 1, st);
+                break;
             case OP_SWEEP_COARSE: level_sweep(C, dt, o.arg ? pf->d_tau : nullptr, st); break;
             case OP_SEND_COARSE: send(w, lc, o.phase, o.iter, st_ptr(C, pf->mc - 1), pf->Kc); break;
             case OP_INTERP_STATES: pair_interp_states(pf->pair, st); break;
@@ -406,7 +415,9 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
             case OP_FAS: pair_fas(pf->pair, dt, pf->d_tau, st); break;
             case OP_INTERP_INC: pair_interp_increment_add(pf->pair, pf->d_dstate0, st); break;
             case OP_RECV_FINE_IC: recv(w, 0, o.phase, o.iter, st_ptr(F, 0), pf->Kf); break;
-            case OP_REFRESH_FINE0: level_refresh(F, 0, 1, st); break;
+            case OP_REFRESH_FINE0:
+                if (!(pf->elide_w0 && w == 0)) level_refresh(F, 0, 1, st);
+                break;
             case OP_INTERP_STATES_MC: pair_interp_states(pf->pair2, st); break;
             case OP_REFRESH_MID_ALL: level_refresh(M, 0, pf->mm, st); break;
             case OP_RESTRICT_MC: pair_restrict_states(pf->pair2, st); break;
@@ -416,7 +427,9 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
             case OP_SEND_MID: send(w, 1, o.phase, o.iter, st_ptr(M, pf->mm - 1), pf->Km); break;
             case OP_INTERP_INC_MC: pair_interp_increment_add(pf->pair2, pf->d_dstate0_mid, st); break;
             case OP_RECV_MID_IC: recv(w, 1, o.phase, o.iter, st_ptr(M, 0), pf->Km); break;
-            case OP_REFRESH_MID0: level_refresh(M, 0, 1, st); break;
+            case OP_REFRESH_MID0:
+                if (!(pf->elide_w0 && w == 0)) level_refresh(M, 0, 1, st);
+                break;
             case OP_FAS_FM: pair_fas(pf->pair, dt, pf->d_tau_mid, st); break;
             default: throw std::logic_error("pfasst: unknown op");
         }
@@ -567,6 +580,7 @@ static void create_serial(pswe_pair* pair, pswe_pair* pair2, const pswe_block_co
     if (!out) throw std::invalid_argument("out is NULL");
     auto* pf = new pswe_pfasst;
     if (const char* e = std::getenv("PSWE_NO_GRAPH")) pf->use_graph = std::atoi(e) == 0;
+    if (const char* e = std::getenv("PSWE_PFASST_NO_ELIDE")) pf->elide_w0 = std::atoi(e) == 0;
     try {
         init_common(pf, pair, cfg, pair2);
         PSWE_CUDA(cudaMalloc(&pf->d_step_final, pf->cfg.n_time_steps * state_bytes(pf->Kf)));
@@ -614,6 +628,7 @@ static void create_dist(pswe_pair* pair, pswe_pair* pair2, const pswe_block_conf
         pf->rank = rank;
         pf->world = world;
         if (const char* e = std::getenv("PSWE_RECV_TIMEOUT")) pf->recv_timeout = std::atof(e);
+        if (const char* e = std::getenv("PSWE_PFASST_NO_ELIDE")) pf->elide_w0 = std::atoi(e) == 0;
         if (const char* e = std::getenv("PSWE_PFASST_FAULT")) pf->fault = std::atoi(e);
         PSWE_CUDA(cudaHostAlloc(&pf->h_err, sizeof(TagError), cudaHostAllocMapped));
         std::memset(pf->h_err, 0, sizeof(TagError));

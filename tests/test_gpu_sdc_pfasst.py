@@ -156,3 +156,22 @@ def test_sweep_emitted_xtiles_bit_identical(tmp_path):
     assert sorted(outs[0].files) == sorted(outs[1].files)
     for k in outs[0].files:
         np.testing.assert_array_equal(outs[0][k], outs[1][k])
+
+
+def test_worker0_refresh_elision_bit_identical(tmp_path):
+    """The executor skips worker 0's node-0 re-evaluations after Steps C/D (its node-0 states never
+    change: pfasst.cpp:152, :175 recompute the same F); results must be bit-identical to running
+    them (PSWE_PFASST_NO_ELIDE=1) - two and three levels, n_ts 1, 2, 4, eager and graph blocks."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ("0", "1"):
+        out = tmp_path / f"pf{env}.npz"
+        subprocess.run([sys.executable, os.path.join(root, "tools", "pfasst_dump.py"), str(out)], check=True,
+                       env={**os.environ, "PSWE_PFASST_NO_ELIDE": env}, timeout=600)
+        outs.append(np.load(out))
+    assert sorted(outs[0].files) == sorted(outs[1].files)
+    for k in outs[0].files:
+        np.testing.assert_array_equal(outs[0][k], outs[1][k])
