@@ -845,7 +845,7 @@ int pswe_pfasst_run_block_steps(pswe_pfasst* pf, const double* theta0, double* s
                                   all.data(), st);
             } catch (const std::exception& e) {
                 pf->broken = true;
-                pf->tr->abort(e.what());
+                pf->tr->abort(e.what(), pf->use_graph && pf->gstream ? pf->gstream : st);
                 throw;
             }
             if (residuals) std::memcpy(residuals, all.data(), sizeof(double) * all.size());

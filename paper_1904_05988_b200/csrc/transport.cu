@@ -137,6 +137,7 @@ struct alignas(64) ShmRank {
     cudaIpcEventHandle_t ev_final;
     alignas(64) std::atomic<unsigned long long> posted[3];  // messages written INTO this rank's rings
     alignas(64) std::atomic<unsigned long long> final_seq;  // blocks whose final this rank published
+    std::atomic<int> abort_ack;  // this rank saw the abort and its stream is drained
     double res[kMaxRes];
 };
 
@@ -217,11 +218,32 @@ public:
         drain_stream(st, timeout_s, [&] { check_abort(); });
     }
 
-    void abort(const std::string& why) override {
+    // Abort handshake: the first failing rank raises the abort word; every rank that sees it
+    // (including the initiator) drains its own stream - so none of its put kernels or peer copies
+    // is still in flight - and acknowledges; the initiator then waits (bounded) for the acks of
+    // its peers before its buffers can go away with the process. A peer that never answers (hung)
+    // only delays the initiator by min(timeout, 10 s).
+    void abort(const std::string& why, cudaStream_t st) override {
         if (!seg_) return;
         int expected = 0;
-        if (seg_->abort_rank.compare_exchange_strong(expected, c_.rank + 1))
-            std::snprintf(seg_->why, sizeof(seg_->why), "%s", why.c_str());
+        const bool initiator = seg_->abort_rank.compare_exchange_strong(expected, c_.rank + 1);
+        if (initiator) std::snprintf(seg_->why, sizeof(seg_->why), "%s", why.c_str());
+        const double wait_s = std::min(timeout_s, 10.0);
+        try {
+            drain_stream(st, wait_s, [] {});
+        } catch (...) {  // a stream stuck for the whole bound: acknowledge anyway
+        }
+        seg_->rank[c_.rank].abort_ack.store(1, std::memory_order_release);
+        if (!initiator) return;
+        const auto deadline = Clock::now() + std::chrono::duration<double>(wait_s);
+        int spins = 0;
+        for (;;) {
+            bool all = true;
+            for (int r = 0; r < c_.world; ++r)
+                if (!seg_->rank[r].abort_ack.load(std::memory_order_acquire)) all = false;
+            if (all || Clock::now() > deadline) break;
+            backoff(spins);
+        }
     }
 
 private:
@@ -326,7 +348,6 @@ private:
     }
 
     void release() {
-        if (seg_) abort_if_unclean();
         for (int r = 0; r < (int)peer_final_.size(); ++r)
             if (r != c_.rank && peer_final_[r]) cudaIpcCloseMemHandle(peer_final_[r]);
         for (int r = 0; r < (int)peer_ev_final_.size(); ++r)
@@ -344,7 +365,6 @@ private:
         if (seg_) munmap(seg_, sizeof(ShmSeg));
         seg_ = nullptr;
     }
-    void abort_if_unclean() {}
 
     void check_abort() {
         const int a = seg_->abort_rank.load(std::memory_order_acquire);
@@ -535,7 +555,7 @@ public:
             PSWE_CUDA(cudaMallocHost(&h_res_all_, sizeof(double) * c.n_res * c.world));
             warm_up();
         } catch (...) {
-            abort("initialisation failed");
+            abort("initialisation failed", nullptr);
             release();
             throw;
         }
@@ -597,12 +617,14 @@ public:
         try {
             drain_stream(st, timeout_s, [&] { poll_async(); });
         } catch (...) {
-            abort("timeout or communicator error");
+            abort("timeout or communicator error", st);
             throw;
         }
     }
 
-    void abort(const std::string&) override {
+    // ncclCommAbort ends every outstanding NCCL operation of this rank; peers' blocked operations
+    // on these communicators then fail and their own drains report it
+    void abort(const std::string&, cudaStream_t) override {
         if (aborted_) return;
         aborted_ = true;
         auto& api = nccl();

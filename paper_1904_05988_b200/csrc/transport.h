@@ -76,8 +76,10 @@ public:
                            const double* d_res_mine, double* res_all, cudaStream_t st) = 0;
     // wait for st with the deadlock guard (throws "pipeline deadlock suspected" after the timeout)
     virtual void drain(cudaStream_t st) = 0;
-    // tell the peers this rank failed (they stop waiting for it)
-    virtual void abort(const std::string& why) = 0;
+    // this rank's block failed: tell the peers (they stop waiting for it), and make sure no GPU
+    // work of any rank still targets another rank's buffers before the processes go away
+    // (st: the stream this rank's block work was issued on; waits are bounded by the timeout)
+    virtual void abort(const std::string& why, cudaStream_t st) = 0;
     double timeout_s = 300.0;
 };
 
