@@ -589,18 +589,24 @@ def run_pfasst(P, prm, world, rank, dev, clocks_dev=0, config=3):
         dist.broadcast_object_list(uid, src=0)
         pf = P.Pfasst(pair, cfg, rank=rank, world=world, uid=uid[0], pair2=pair2, transport=transport)
     theta0 = torch.as_tensor(config_state(config, plans[0])).to(dev)
-    P.run_blocks(pf, theta0, 1)  # warm-up block (also captures the serial-emulation graph)
+    # warm-up: an eager block, then the block whose launches are captured into CUDA graphs (serial
+    # emulation: the whole block; distributed: segment graphs) - neither inside the timed region
+    P.run_blocks(pf, theta0, 2)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    fin, hist = P.run_blocks(pf, theta0, n_blocks)
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b)
-    if world > 1:
-        ms = max_over_ranks(ms, dev)
+    runs = []
+    for _ in range(3):  # the whole config (all its steps) three times; the median is reported
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fin, hist = P.run_blocks(pf, theta0, n_blocks)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        if world > 1:
+            ms = max_over_ranks(ms, dev)
+        runs.append(ms)
+    ms = sorted(runs)[1]
     wall = ms * 1e-3
     desc = "/".join(f"T{R}({nlat}x{nlon})" for R, nlat, nlon, _ in lv)
     nodes = "/".join(str(nn) for *_, nn in lv)
@@ -608,6 +614,7 @@ def run_pfasst(P, prm, world, rank, dev, clocks_dev=0, config=3):
     return {"config": f"config {config}: {desc}, {nodes} nodes, dt {dt:g} s, {steps} steps, {n_iter} iterations",
             "levels": len(lv), "n_ts": world, "blocks": n_blocks, "wall_s": wall,
             "wall_s_per_sim_day": wall / (steps * dt) * 86400,
+            "timing": "median of 3 runs of all steps, after an eager and a graph-capture warm-up block",
             "final_residuals": [float(r) for r in hist[-1][:, -1]],
             "_theta0": theta0.cpu().numpy() if config == 3 else None}
 

@@ -36,7 +36,7 @@ void level_residual(pswe_level* L, double dt, double* out, cudaStream_t st);
 void pair_restrict_states(pswe_pair* P, cudaStream_t st);
 void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st, const double2* tau_f = nullptr);
 void pair_save(pswe_pair* P, cudaStream_t st);
-void pair_interp_increment_add(pswe_pair* P, double2* dstate0, cudaStream_t st);
+void pair_interp_increment_add(pswe_pair* P, double2* dstate0, cudaStream_t st, bool dstate0_outside_zero);
 void pair_interp_states(pswe_pair* P, cudaStream_t st);
 }  // namespace pswe
 
@@ -300,6 +300,8 @@ void init_common(pswe_pfasst* pf, pswe_pair* pair, const pswe_block_config* cfg,
         pf->Km = num_coeffs(pf->Rm);
         PSWE_CUDA(cudaMalloc(&pf->d_tau_mid, pf->mm * state_bytes(pf->Km)));
         PSWE_CUDA(cudaMalloc(&pf->d_dstate0_mid, state_bytes(pf->Km)));
+        // increments are written only inside the coarser triangle: the rest stays zero
+        PSWE_CUDA(cudaMemset(pf->d_dstate0_mid, 0, state_bytes(pf->Km)));
     }
     pf->Rf = pf->fine->R;
     pf->mf = pf->fine->nn;
@@ -309,6 +311,7 @@ void init_common(pswe_pfasst* pf, pswe_pair* pair, const pswe_block_config* cfg,
     pf->Kc = num_coeffs(pf->Rc);
     PSWE_CUDA(cudaMalloc(&pf->d_tau, pf->mc * state_bytes(pf->Kc)));
     PSWE_CUDA(cudaMalloc(&pf->d_dstate0, state_bytes(pf->Kf)));
+    PSWE_CUDA(cudaMemset(pf->d_dstate0, 0, state_bytes(pf->Kf)));
     PSWE_CUDA(cudaMalloc(&pf->d_res, sizeof(double) * cfg->n_time_steps * (cfg->n_iter + 1)));
 }
 
@@ -413,7 +416,7 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
             case OP_REFRESH_COARSE_ALL: level_refresh(C, 0, pf->mc, st); break;
             case OP_SAVE: pair_save(pf->pair, st); break;
             case OP_FAS: pair_fas(pf->pair, dt, pf->d_tau, st); break;
-            case OP_INTERP_INC: pair_interp_increment_add(pf->pair, pf->d_dstate0, st); break;
+            case OP_INTERP_INC: pair_interp_increment_add(pf->pair, pf->d_dstate0, st, true); break;
             case OP_RECV_FINE_IC: recv(w, 0, o.phase, o.iter, st_ptr(F, 0), pf->Kf); break;
             case OP_REFRESH_FINE0:
                 if (!(pf->elide_w0 && w == 0)) level_refresh(F, 0, 1, st);
@@ -425,7 +428,7 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
             case OP_FAS_MC: pair_fas(pf->pair2, dt, pf->d_tau, st, pf->d_tau_mid); break;
             case OP_SWEEP_MID: level_sweep(M, dt, pf->d_tau_mid, st); break;
             case OP_SEND_MID: send(w, 1, o.phase, o.iter, st_ptr(M, pf->mm - 1), pf->Km); break;
-            case OP_INTERP_INC_MC: pair_interp_increment_add(pf->pair2, pf->d_dstate0_mid, st); break;
+            case OP_INTERP_INC_MC: pair_interp_increment_add(pf->pair2, pf->d_dstate0_mid, st, true); break;
             case OP_RECV_MID_IC: recv(w, 1, o.phase, o.iter, st_ptr(M, 0), pf->Km); break;
             case OP_REFRESH_MID0:
                 if (!(pf->elide_w0 && w == 0)) level_refresh(M, 0, 1, st);

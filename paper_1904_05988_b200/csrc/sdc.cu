@@ -510,6 +510,49 @@ __global__ void interp_kernel(InterpArgs A, int mode) {
     }
 }
 
+// interpolate_increment_add restricted to the coefficients that can change: the increment is the
+// zero-padded coarse difference, so fine coefficients outside the coarse triangle (3/4 of them for
+// T255 -> T127) receive exactly zero - the full-range kernel above read and rewrote them anyway.
+// One thread per (coarse coefficient, field); blockIdx.y = fam * mf + i. dstate0 (optional) gets
+// the node-0 state increment inside the triangle; zero_out_kernel writes its zeros outside.
+__global__ void interp_inc_kernel(InterpArgs A) {
+    const long Kc = (long)(A.Rc + 1) * (A.Rc + 2) / 2, Kf = (long)(A.Rf + 1) * (A.Rf + 2) / 2;
+    const long kc3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int fam = blockIdx.y / A.mf, i = blockIdx.y - fam * A.mf;
+    pdl_trigger();
+    pdl_wait();
+    if (kc3 >= 3 * Kc) return;
+    const int f = (int)(kc3 / Kc);
+    const long kc = kc3 - f * Kc;
+    int m, s;
+    decode_rs(A.Rc, kc, m, s);
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < kMaxNodes; ++j) {
+        const double w = A.w[i][j];
+        if (j < A.mc && w != 0.0) {
+            const double2 a = A.a[fam][j][kc3], b = A.b[fam][j][kc3];
+            axpy(acc, w, make_double2(a.x - b.x, a.y - b.y));
+        }
+    }
+    const long kf3 = f * Kf + off_std(A.Rf, m) + (s - m);
+    double2* o = A.dst[fam][i] + kf3;
+    const double2 cur = *o;
+    *o = make_double2(cur.x + acc.x, cur.y + acc.y);
+    if (fam == 0 && i == 0 && A.dstate0) A.dstate0[kf3] = acc;
+}
+
+__global__ void zero_out_kernel(int Rf, int Rc, double2* __restrict__ y) {
+    const long Kf = (long)(Rf + 1) * (Rf + 2) / 2;
+    const long kf3 = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_trigger();
+    pdl_wait();
+    if (kf3 >= 3 * Kf) return;
+    int m, s;
+    decode_rs(Rf, kf3 % Kf, m, s);
+    if (m > Rc || s > Rc) y[kf3] = make_double2(0.0, 0.0);
+}
+
 }  // namespace
 }  // namespace pswe
 
@@ -692,7 +735,7 @@ void pair_save(pswe_pair* P, cudaStream_t st) {
            (long)C->nn * 3 * C->K, st);
 }
 
-void pair_interp_increment_add(pswe_pair* P, double2* dstate0, cudaStream_t st) {
+void pair_interp_increment_add(pswe_pair* P, double2* dstate0, cudaStream_t st, bool dstate0_outside_zero) {
     pswe_level *F = P->fine, *C = P->coarse;
     InterpArgs A{};
     A.mf = F->nn;
@@ -713,9 +756,21 @@ void pair_interp_increment_add(pswe_pair* P, double2* dstate0, cudaStream_t st) 
         A.dst[2][i] = F->fe(i);
         for (int j = 0; j < C->nn; ++j) A.w[i][j] = P->ti[(size_t)i * C->nn + j];
     }
-    const long n = 3 * F->K;
-    launch_pdl(interp_kernel, dim3((unsigned)((n + 127) / 128), 3 * F->nn), dim3(128), 0, st, A, 0);
+    static const bool full = [] { const char* e = getenv("PSWE_INTERP_FULL"); return e && atoi(e) != 0; }();
+    if (full) {  // A/B: the full-range kernel
+        const long n = 3 * F->K;
+        launch_pdl(interp_kernel, dim3((unsigned)((n + 127) / 128), 3 * F->nn), dim3(128), 0, st, A, 0);
+        PSWE_LAUNCH_CHECK();
+        return;
+    }
+    const long nc = 3 * C->K;
+    launch_pdl(interp_inc_kernel, dim3((unsigned)((nc + 127) / 128), 3 * F->nn), dim3(128), 0, st, A);
     PSWE_LAUNCH_CHECK();
+    if (dstate0 && !dstate0_outside_zero && F->R > C->R) {
+        const long n = 3 * F->K;
+        launch_pdl(zero_out_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, F->R, C->R, dstate0);
+        PSWE_LAUNCH_CHECK();
+    }
 }
 
 void pair_interp_states(pswe_pair* P, cudaStream_t st) {
@@ -982,7 +1037,7 @@ int pswe_save_coarse(pswe_pair* P, void* stream) {
 int pswe_interpolate_increment_add(pswe_pair* P, double* dstate0, void* stream) {
     return guarded([&] {
         if (!P) throw std::invalid_argument("NULL pair");
-        pair_interp_increment_add(P, reinterpret_cast<double2*>(dstate0), as_stream(stream));
+        pair_interp_increment_add(P, reinterpret_cast<double2*>(dstate0), as_stream(stream), false);
     });
 }
 
