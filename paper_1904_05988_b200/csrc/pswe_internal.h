@@ -298,6 +298,7 @@ struct pswe_level {
     unsigned long long* d_res = nullptr;
     unsigned long long* d_bmax = nullptr;  // residual: per-block maxima
     unsigned int* d_count = nullptr;       // residual: blocks done (0 between launches)
+    double2* d_qsum = nullptr;             // sweep: quadrature of the old right-hand sides, [nn-2][3K]
     double2* st(int node) const { return d_state + (size_t)node * 3 * K; }
     double2* fi(int node, int buf = -1) const { return d_f[buf < 0 ? cur : buf][0] + (size_t)node * 3 * K; }
     double2* fe(int node, int buf = -1) const { return d_f[buf < 0 ? cur : buf][1] + (size_t)node * 3 * K; }

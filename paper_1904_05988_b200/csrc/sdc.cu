@@ -117,6 +117,12 @@ struct SweepNodeArgs {
     double ae[kMaxNodes], ai[kMaxNodes];  // dt*qE(m+1,j), dt*qI(m+1,j), j = 1..m
     double aq[kMaxNodes];                 // dt*q(m+1,j), j = 0..M
     double aii;                           // dt*qI(m+1,m+1)
+    // quadrature of the OLD right-hand sides, S_m = sum_j dt q(m+1,j) (F_I^old_j + F_E^old_j): the same
+    // ten arrays for every node of the sweep, so the first node's kernel (which reads them anyway)
+    // forms S_1 .. S_{M-1} for the later nodes, which read one array instead of ten
+    double aq_all[kMaxNodes][kMaxNodes];  // first node: dt*q(m'+1, j) for m' = 1..M-1
+    double2* qsum_out;                    // first node: S_1 .. S_{M-1}, [M-1][3K]
+    const double2* qsum_in;               // later nodes: S_m (or nullptr: the ten-array sum)
     double2* fi0_dst;                     // node 0's F_I, F_E copied old -> new buffer (first node only)
     double2* fe0_dst;
     const double2* proj;                  // fused tail: projections of state m ([5][Kx]), the state,
@@ -213,14 +219,38 @@ __global__ void __launch_bounds__(XP ? 390 : 384) sweep_node_kernel(SweepNodeArg
             }
         }
         axpy(acc, -A.aii, A.fi_old[A.m + 1][i]);
+        if (A.qsum_in) {
+            const double2 q = A.qsum_in[i];
+            acc.x += q.x;
+            acc.y += q.y;
+        } else {
+            double2 qs[NN];  // S_{m'} of the later nodes (first node only)
 #pragma unroll
-        for (int j = 0; j < NN; ++j) {
-            const double2 fij = A.fi_old[j][i], fej = A.fe_old[j][i];
-            axpy(acc, A.aq[j], fij);
-            axpy(acc, A.aq[j], fej);
-            if (j == 0 && A.fi0_dst && owned) {  // node 0 keeps its right-hand sides (sdc.cpp:22-29)
-                A.fi0_dst[i] = fij;
-                A.fe0_dst[i] = fej;
+            for (int mm = 0; mm < NN; ++mm) qs[mm] = make_double2(0.0, 0.0);
+            double2 qm = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < NN; ++j) {
+                const double2 fij = A.fi_old[j][i], fej = A.fe_old[j][i];
+                axpy(qm, A.aq[j], fij);
+                axpy(qm, A.aq[j], fej);
+                if (A.qsum_out) {
+#pragma unroll
+                    for (int mm = 1; mm < NN - 1; ++mm) {
+                        axpy(qs[mm], A.aq_all[mm][j], fij);
+                        axpy(qs[mm], A.aq_all[mm][j], fej);
+                    }
+                }
+                if (j == 0 && A.fi0_dst && owned) {  // node 0 keeps its right-hand sides (sdc.cpp:22-29)
+                    A.fi0_dst[i] = fij;
+                    A.fe0_dst[i] = fej;
+                }
+            }
+            acc.x += qm.x;
+            acc.y += qm.y;
+            if (A.qsum_out && owned) {
+#pragma unroll
+                for (int mm = 1; mm < NN - 1; ++mm)
+                    if (mm < A.M) A.qsum_out[(size_t)(mm - 1) * 3 * K + i] = qs[mm];
             }
         }
         if (A.tau) {
@@ -627,6 +657,15 @@ void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) 
             }
         }
         A.aii = dt * t.QI(m + 1, m + 1);
+        if (L->d_qsum && M >= 2) {
+            if (m == 0) {
+                A.qsum_out = L->d_qsum;
+                for (int mm = 1; mm < M; ++mm)
+                    for (int j = 0; j <= M; ++j) A.aq_all[mm][j] = dt * t.Q(mm + 1, j);
+            } else {
+                A.qsum_in = L->d_qsum + (size_t)(m - 1) * 3 * L->K;
+            }
+        }
         A.fi0_dst = m == 0 ? L->fi(0, nw) : nullptr;
         A.fe0_dst = m == 0 ? L->fe(0, nw) : nullptr;
         A.m = m;
@@ -855,9 +894,13 @@ int pswe_level_create(pswe_plan* plan, const pswe_params* p, int num_nodes, pswe
             PSWE_CUDA(cudaMalloc(&L->d_bmax, nblk * sizeof(unsigned long long)));
             PSWE_CUDA(cudaMalloc(&L->d_count, sizeof(unsigned int)));
             PSWE_CUDA(cudaMemset(L->d_count, 0, sizeof(unsigned int)));
+            static const bool qsum_off = [] { const char* e = getenv("PSWE_NO_QSUM"); return e && atoi(e) != 0; }();
+            if (num_nodes >= 4 && !qsum_off)
+                PSWE_CUDA(cudaMalloc(&L->d_qsum, (size_t)(num_nodes - 2) * 3 * L->K * sizeof(double2)));
             plan->reserve(num_nodes);
         } catch (...) {
             if (L->d_state) cudaFree(L->d_state);
+            if (L->d_qsum) cudaFree(L->d_qsum);
             if (L->d_bmax) cudaFree(L->d_bmax);
             if (L->d_count) cudaFree(L->d_count);
             for (auto& b : L->d_f)
@@ -876,6 +919,7 @@ int pswe_level_destroy(pswe_level* L) {
         cudaFree(L->d_state);
         if (L->d_bmax) cudaFree(L->d_bmax);
         if (L->d_count) cudaFree(L->d_count);
+        if (L->d_qsum) cudaFree(L->d_qsum);
         for (auto& b : L->d_f)
             for (auto* q : b) cudaFree(q);
         delete L;
