@@ -31,7 +31,7 @@
 namespace pswe {
 void level_spread(pswe_level* L, const double2* theta0, cudaStream_t st);
 void level_refresh(pswe_level* L, int first, int count, cudaStream_t st);
-void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st);
+void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st, double* res_out = nullptr);
 void level_residual(pswe_level* L, double dt, double* out, cudaStream_t st);
 void pair_restrict_states(pswe_pair* P, cudaStream_t st);
 void pair_fas(pswe_pair* P, double dt, double2* tau, cudaStream_t st, const double2* tau_f = nullptr);
@@ -385,6 +385,9 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
         "INTERP_INC", "RECV_FINE_IC", "REFRESH_FINE0", "INTERP_STATES_MC", "REFRESH_MID_ALL", "RESTRICT_MC",
         "SAVE_MC", "FAS_MC", "SWEEP_MID", "SEND_MID", "INTERP_INC_MC", "RECV_MID_IC", "REFRESH_MID0", "FAS_FM"};
     const std::vector<Op> ops = build_schedule(w, n, N, pf->nlev, pf->mid_sweeps);
+    // a fine sweep followed by the residual: its last tail kernel computes the residual too
+    static const bool fuse_res = [] { const char* e = getenv("PSWE_NO_TAIL_RES"); return !(e && atoi(e) != 0); }();
+    bool res_fused = false;
     for (size_t i = 0; i < ops.size(); ++i) {
         const Op& o = ops[i];
         PSWE_NVTX(op_name[o.code]);
@@ -409,8 +412,21 @@ void run_worker(pswe_pfasst* pf, int w, const double2* theta0, cudaStream_t st, 
             case OP_SEND_COARSE: send(w, lc, o.phase, o.iter, st_ptr(C, pf->mc - 1), pf->Kc); break;
             case OP_INTERP_STATES: pair_interp_states(pf->pair, st); break;
             case OP_REFRESH_FINE_ALL: level_refresh(F, 0, pf->mf, st); break;
-            case OP_RESIDUAL: level_residual(F, dt, pf->d_res + (size_t)w * (N + 1) + o.arg, st); break;
-            case OP_SWEEP_FINE: level_sweep(F, dt, nullptr, st); break;
+            case OP_RESIDUAL:
+                if (res_fused) {  // computed by the preceding sweep's last kernel
+                    res_fused = false;
+                    break;
+                }
+                level_residual(F, dt, pf->d_res + (size_t)w * (N + 1) + o.arg, st);
+                break;
+            case OP_SWEEP_FINE: {
+                double* r = nullptr;
+                if (fuse_res && i + 1 < ops.size() && ops[i + 1].code == OP_RESIDUAL)
+                    r = pf->d_res + (size_t)w * (N + 1) + ops[i + 1].arg;
+                level_sweep(F, dt, nullptr, st, r);
+                res_fused = r != nullptr;
+                break;
+            }
             case OP_SEND_FINE: send(w, 0, o.phase, o.iter, st_ptr(F, pf->mf - 1), pf->Kf); break;
             case OP_RESTRICT: pair_restrict_states(pf->pair, st); break;
             case OP_REFRESH_COARSE_ALL: level_refresh(C, 0, pf->mc, st); break;

@@ -330,63 +330,116 @@ struct ResidualArgs {
     unsigned int* count;       // blocks done; the last block reduces and resets it to 0
 };
 
-// F_I, F_E of every node loaded once per coefficient and reused for all NN rows (same axpy order)
-template <int NN>
-__global__ void residual_kernel(ResidualArgs A, unsigned long long* out) {
-    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    pdl_trigger();
-    pdl_wait();
-    double mx = 0.0;
-    if (i < A.n3) {
-        double2 fi[NN], fe[NN], st[NN];
+// collocation residual of flat index i (sdc.cpp:46-62): F_I, F_E of every node loaded once and
+// reused for all NN rows (same axpy order). LAST: node NN-1's right-hand sides come from registers.
+template <int NN, bool LAST>
+__device__ __forceinline__ double residual_at(const ResidualArgs& A, long i, double2 fi_last, double2 fe_last) {
+    double2 fi[NN], fe[NN], st[NN];
 #pragma unroll
-        for (int j = 0; j < NN; ++j) {
+    for (int j = 0; j < NN; ++j) {
+        if (LAST && j == NN - 1) {
+            fi[j] = fi_last;
+            fe[j] = fe_last;
+        } else {
             fi[j] = A.fi[j][i];
             fe[j] = A.fe[j][i];
-            st[j] = A.state[j][i];
         }
-        const double2 s0 = st[0];
-#pragma unroll
-        for (int m = 0; m < NN; ++m) {
-            double2 acc = make_double2(st[m].x - s0.x, st[m].y - s0.y);
-#pragma unroll
-            for (int j = 0; j < NN; ++j) {
-                axpy(acc, A.w[m][j], fi[j]);
-                axpy(acc, A.w[m][j], fe[j]);
-            }
-            mx = fmax(mx, hypot(acc.x, acc.y));
-        }
+        st[j] = A.state[j][i];
     }
-    // block max
+    const double2 s0 = st[0];
+    double mx = 0.0;
+#pragma unroll
+    for (int m = 0; m < NN; ++m) {
+        double2 acc = make_double2(st[m].x - s0.x, st[m].y - s0.y);
+#pragma unroll
+        for (int j = 0; j < NN; ++j) {
+            axpy(acc, A.w[m][j], fi[j]);
+            axpy(acc, A.w[m][j], fe[j]);
+        }
+        mx = fmax(mx, hypot(acc.x, acc.y));
+    }
+    return mx;
+}
+
+// block max, then the last block to finish reduces the block maxima (max is order-independent, so
+// the result is deterministic whatever the block shape) - no zeroing of *out beforehand
+__device__ __forceinline__ void residual_finish(double mx, const ResidualArgs& A, unsigned long long* out) {
+    const unsigned tid = threadIdx.x + threadIdx.y * blockDim.x;
+    const unsigned nthr = blockDim.x * blockDim.y;
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     __shared__ double wm[32];
-    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+    if ((tid & 31) == 0) wm[tid >> 5] = mx;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        mx = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0.0;
+    if (tid < 32) {
+        mx = tid < (nthr >> 5) ? wm[tid] : 0.0;
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             A.bmax[blockIdx.x] = (unsigned long long)__double_as_longlong(mx);
             __threadfence();
             wm[0] = atomicAdd(A.count, 1u) == gridDim.x - 1 ? 1.0 : 0.0;
         }
     }
-    // the last block to finish reduces the block maxima (max is order-independent, so the result
-    // is deterministic) - no zeroing of *out beforehand
     __syncthreads();
     if (wm[0] == 0.0) return;
     __threadfence();
     unsigned long long b = 0ull;
-    for (unsigned j = threadIdx.x; j < gridDim.x; j += blockDim.x) b = max(b, __ldcg(A.bmax + j));
+    for (unsigned j = tid; j < gridDim.x; j += nthr) b = max(b, __ldcg(A.bmax + j));
     for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
     __shared__ unsigned long long wb[32];
-    if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = b;
+    if ((tid & 31) == 0) wb[tid >> 5] = b;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b = max(b, wb[w]);
+    if (tid == 0) {
+        for (int w = 1; w < (int)(nthr >> 5); ++w) b = max(b, wb[w]);
         *out = b;
         *A.count = 0u;
     }
+}
+
+template <int NN>
+__global__ void residual_kernel(ResidualArgs A, unsigned long long* out) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_trigger();
+    pdl_wait();
+    const double2 z = make_double2(0.0, 0.0);
+    const double mx = i < A.n3 ? residual_at<NN, false>(A, i, z, z) : 0.0;
+    residual_finish(mx, A, out);
+}
+
+// the sweep's last evaluation tail (eval_tail_kernel's expressions, tail.cuh) fused with the
+// collocation residual that follows it in the PFASST schedule (pfasst.cpp OP_SWEEP_FINE +
+// OP_RESIDUAL): block (128, 3), thread (x, f) finishes field f of coefficient k of the last node,
+// stores it and takes it from registers into that index's residual rows - one launch and one
+// round trip of F[M] fewer; every value is the one the two separate kernels produce
+template <int NN>
+__global__ void __launch_bounds__(384) tail_residual_kernel(ResidualArgs A, const double* __restrict__ eps,
+                                                            const double2* __restrict__ proj,
+                                                            double2* __restrict__ fi_last,
+                                                            double2* __restrict__ fe_last, int R, double inv_a2,
+                                                            double phi_bar, double nu, unsigned long long* out) {
+    const long K = (long)(R + 1) * (R + 2) / 2;
+    const long Kx = (long)(R + 1) * (R + 4) / 2;
+    const long k = (long)blockIdx.x * 128 + threadIdx.x;
+    const int f = threadIdx.y;
+    pdl_trigger();
+    int m = 0, s = 0;
+    double eu = 0.0, el = 0.0;
+    if (k < K) {
+        decode_rs(R, k, m, s);
+        eu = eps[off_ext(R, m) + s - m + 1];
+        el = eps[off_ext(R, m) + s - m];
+    }
+    pdl_wait();  // the projections come from the forward Legendre kernel
+    double mx = 0.0;
+    if (k < K) {
+        double2 e, i;
+        tailc::tail_field(f, eu, el, proj, Kx, off_ext(R, m), m, s, -s * (s + 1.0) * inv_a2, A.state[NN - 1], K, k,
+                          phi_bar, nu, true, e, i);
+        const long ix = f * K + k;
+        fe_last[ix] = e;
+        fi_last[ix] = i;
+        mx = residual_at<NN, true>(A, ix, i, e);
+    }
+    residual_finish(mx, A, out);
 }
 
 struct CopyArgs {
@@ -626,7 +679,22 @@ void level_spread(pswe_level* L, const double2* theta0, cudaStream_t st) {
 
 void level_refresh(pswe_level* L, int first, int count, cudaStream_t st) { refresh(L, first, count, st); }
 
-void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) {
+static ResidualArgs residual_args(pswe_level* L, double dt, int set) {
+    ResidualArgs A{};
+    A.nn = L->nn;
+    A.n3 = 3 * L->K;
+    for (int m = 0; m < L->nn; ++m) {
+        A.state[m] = L->st(m);
+        A.fi[m] = L->fi(m, set);
+        A.fe[m] = L->fe(m, set);
+        for (int j = 0; j < L->nn; ++j) A.w[m][j] = -dt * L->tab.Q(m, j);
+    }
+    A.bmax = L->d_bmax;
+    A.count = L->d_count;
+    return A;
+}
+
+void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st, double* res_out) {
     const int M = L->nn - 1;
     const int old = L->cur, nw = 1 - L->cur;
     const size_t bytes = 3 * L->K * sizeof(double2);
@@ -700,24 +768,32 @@ void level_sweep(pswe_level* L, double dt, const double2* tau, cudaStream_t st) 
         PSWE_LAUNCH_CHECK();
         eval_imex_proj(*L->plan, L->prm, L->st(m + 1), 1, st, xp);
     }
-    eval_tail(*L->plan, L->prm, L->plan->d_proj, L->st(M), L->fi(M, nw), L->fe(M, nw), 1, st);
+    if (res_out) {  // the last node's tail and the residual after the sweep in one launch
+        const ResidualArgs A = residual_args(L, dt, nw);
+        const dim3 grid((unsigned)((L->K + 127) / 128)), block(128, 3);
+        auto* o = reinterpret_cast<unsigned long long*>(res_out);
+        const pswe_plan& P = *L->plan;
+        const double ia2 = 1.0 / (L->prm.radius * L->prm.radius);
+#define PSWE_TR_LAUNCH(NN)                                                                                  \
+    launch_pdl(tail_residual_kernel<NN>, grid, block, 0, st, A, P.d_eps, P.d_proj, L->fi(M, nw), L->fe(M, nw), \
+               L->R, ia2, L->prm.phi_bar, L->prm.nu, o);
+        switch (L->nn) {
+            case 2: PSWE_TR_LAUNCH(2) break;
+            case 3: PSWE_TR_LAUNCH(3) break;
+            default: PSWE_TR_LAUNCH(5) break;
+        }
+#undef PSWE_TR_LAUNCH
+        PSWE_LAUNCH_CHECK();
+    } else {
+        eval_tail(*L->plan, L->prm, L->plan->d_proj, L->st(M), L->fi(M, nw), L->fe(M, nw), 1, st);
+    }
     L->cur = nw;
 }
 
 void level_residual(pswe_level* L, double dt, double* out, cudaStream_t st) {
-    ResidualArgs A{};
-    A.nn = L->nn;
-    A.n3 = 3 * L->K;
-    for (int m = 0; m < L->nn; ++m) {
-        A.state[m] = L->st(m);
-        A.fi[m] = L->fi(m);
-        A.fe[m] = L->fe(m);
-        for (int j = 0; j < L->nn; ++j) A.w[m][j] = -dt * L->tab.Q(m, j);
-    }
+    const ResidualArgs A = residual_args(L, dt, L->cur);
     const int bs = 256;
     const unsigned g = (unsigned)((A.n3 + bs - 1) / bs);
-    A.bmax = L->d_bmax;
-    A.count = L->d_count;
     auto* o = reinterpret_cast<unsigned long long*>(out);
     switch (L->nn) {
         case 2: launch_pdl(residual_kernel<2>, dim3(g), dim3(bs), 0, st, A, o); break;
@@ -965,7 +1041,7 @@ int pswe_sweep(pswe_level* L, double dt, const double* tau, void* stream) {
     PSWE_NVTX("pswe.sweep");
     return guarded([&] {
         if (!L) throw std::invalid_argument("NULL level");
-        level_sweep(L, dt, reinterpret_cast<const double2*>(tau), as_stream(stream));
+        level_sweep(L, dt, reinterpret_cast<const double2*>(tau), as_stream(stream), nullptr);
     });
 }
 
@@ -983,8 +1059,8 @@ int pswe_sdc_step(pswe_level* L, const double* theta0, double dt, int n_sweeps, 
         if (!L || !theta0) throw std::invalid_argument("NULL argument");
         const cudaStream_t st = as_stream(stream);
         level_spread(L, reinterpret_cast<const double2*>(theta0), st);
-        for (int k = 0; k < n_sweeps; ++k) level_sweep(L, dt, nullptr, st);
-        if (out_res) level_residual(L, dt, out_res, st);
+        for (int k = 0; k < n_sweeps; ++k) level_sweep(L, dt, nullptr, st, k == n_sweeps - 1 ? out_res : nullptr);
+        if (out_res && n_sweeps == 0) level_residual(L, dt, out_res, st);
     });
 }
 
