@@ -93,6 +93,11 @@ int pswe_analyse(pswe_plan* P, const double* grid, double* coeffs, int n, void* 
         need(grid, "grid", n);
         if (n <= 0) return;
         P->reserve(batch_groups(n, 5));
+        const GtLayout gl = gt_layout_fields(P->R, P->J, n);
+        if (analyse_gt_ok(*P, gl) && fft_r2c_gt(*P, grid, gl, n, as_stream(stream))) {
+            legendre_forward_fields_gt(*P, gl, n, c2(coeffs), as_stream(stream));
+            return;
+        }
         fft_rows_r2c(*P, grid, P->d_four_a, 1, 0, n, false, 0, 1.0, as_stream(stream));
         legendre_forward(*P, P->d_four_a, n, 1, c2(coeffs), false, as_stream(stream));
     });

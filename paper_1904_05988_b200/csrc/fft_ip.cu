@@ -31,6 +31,7 @@ namespace {
 constexpr int kIpThreads = 256;
 
 
+
 // radix of pass s (0 = first) of the in-place plan for length N; 0 past the last pass.
 // Plans: head(N/8) then a final radix-8 pass.
 // Plan pl = 1 (narrow evaluations and the plain row transforms): N = 256 as two radix-16 passes
@@ -417,13 +418,15 @@ __host__ __device__ constexpr int ip_rows(int N) { return N <= 512 ? 8 : (N <= 1
 // R2C: grid rows (optionally * cos) -> forward DIF passes -> r2c post-pass gathered from the
 //      digit-reversed slots, scaled (scale_mode 0: w / nlon, 1: w / (a cos^2 nlon)), staged
 //      [m][row] in shared memory -> Fourier rows [q][m][i] (q = b out_stride + out_off).
-template <int N, bool C2R>
+// (c2r at N = 256 takes 96 registers, two blocks per SM; capping it at three blocks spills and
+// measured no faster, r2aw)
+template <int N, bool C2R, int ROWS>
 __global__ void __launch_bounds__(kIpThreads)
     fft_rows_ip_kernel(int R, int nlat, const double2* __restrict__ TW, const double2* __restrict__ post,
                        const double2* __restrict__ four_in, const double* __restrict__ grid_in, double2* __restrict__ four_out,
                        double* __restrict__ grid_out, int stride, int off, const double* __restrict__ rowc,
                        const double* __restrict__ roww, int cos_flag, int scale_mode, double inv_a) {
-    constexpr int ROWS = ip_rows(N), RS = ipadded(N);
+    constexpr int RS = ipadded(N);
     extern __shared__ double2 A[];  // [ROWS][N] ipad layout (R2C: then the [R+1][ROWS] staging); twiddles
     double2* sTW = A + ROWS * RS;
     const int i0 = blockIdx.x * ROWS, b = blockIdx.y;
@@ -534,13 +537,12 @@ __global__ void __launch_bounds__(kIpThreads)
     }
 }
 
-template <int N, bool C2R>
-bool rows_ip(const pswe_plan& P, const double2* four_in, const double* grid_in, double2* four_out, double* grid_out,
-             int stride, int off, int n, int cos_flag, int scale_mode, double inv_a, cudaStream_t st) {
-    constexpr int ROWS = ip_rows(N);
+template <int N, bool C2R, int ROWS>
+bool rows_ip_r(const pswe_plan& P, const double2* four_in, const double* grid_in, double2* four_out, double* grid_out,
+               int stride, int off, int n, int cos_flag, int scale_mode, double inv_a, cudaStream_t st) {
     const size_t sm = (size_t)(ROWS * ipadded(N) + ip_ntw(N, 1)) * sizeof(double2);  // plan 1
     if (sm > 227 * 1024) return false;
-    auto kern = fft_rows_ip_kernel<N, C2R>;
+    auto kern = fft_rows_ip_kernel<N, C2R, ROWS>;
     static bool attr = false;  // once per instantiation (the cap, not the size of this launch)
     if (!attr) {
         PSWE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -553,7 +555,128 @@ bool rows_ip(const pswe_plan& P, const double2* four_in, const double* grid_in, 
     return true;
 }
 
+template <int N, bool C2R>
+bool rows_ip(const pswe_plan& P, const double2* four_in, const double* grid_in, double2* four_out, double* grid_out,
+             int stride, int off, int n, int cos_flag, int scale_mode, double inv_a, cudaStream_t st) {
+    // (4 or 2 latitude rows per block measured slower at N = 256, r2au: c2r 13.5 -> 14.5 / 18.7 us)
+    return rows_ip_r<N, C2R, ip_rows(N)>(P, four_in, grid_in, four_out, grid_out, stride, off, n, cos_flag, scale_mode,
+                                         inv_a, st);
+}
+
+// analyse's longitude transforms on the forward-Legendre G tiles (transform.cpp:163-174 with the
+// Fourier coefficients written where the streamed forward reads them, gt_layout_fields): block =
+// (latitude row i, 8 fields f0..f0+7), the rows of fft_rows_ip_kernel<N, false> being 8 FIELDS
+// of one latitude instead of 8 latitudes of one field, so each order m's (re, im) pairs of the
+// block's fields are one 128-byte run of a G-tile row (the column swizzle moves 32-byte groups).
+// Same passes, post-pass and scaling (w_i / nlon) as the row kernel.
+template <int N>
+__global__ void __launch_bounds__(kIpThreads)
+    fft_r2c_gt_kernel(int R, int nlat, int nf, const double2* __restrict__ TW, const double2* __restrict__ post,
+                      const double* __restrict__ grid_in, double* __restrict__ gtile, const double* __restrict__ roww,
+                      GtLayout gl) {
+    constexpr int ROWS = 8, RS = ipadded(N);
+    extern __shared__ double2 A[];  // [ROWS][N] ipad layout, then the [R+1][ROWS] staging; twiddles
+    double2* sTW = A + ROWS * RS;
+    const int i = blockIdx.x, f0 = blockIdx.y * ROWS;
+    const int nrow = min(ROWS, nf - f0);
+    pdl_trigger();  // the forward's P-tile prologue overlaps this kernel (it waits before the G reads)
+    for (int t = threadIdx.x; t < ip_ntw(N, 1); t += kIpThreads) {
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sTW + t));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(TW + t));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    constexpr int UL = (ROWS * N + kIpThreads - 1) / kIpThreads;
+    double2 v[UL];
+#pragma unroll
+    for (int u = 0; u < UL; ++u) {
+        const int it = threadIdx.x + u * kIpThreads;
+        const int r = it / N, e = it - r * N;
+        v[u] = r < nrow && it < ROWS * N ? reinterpret_cast<const double2*>(grid_in + ((long)(f0 + r) * nlat + i) * 2 * N)[e]
+                        : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < UL; ++u)
+        if (threadIdx.x + u * kIpThreads < ROWS * N) A[ipad(threadIdx.x + u * kIpThreads)] = v[u];
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    DifGuard<N, 0, ROWS, false, 1>::run(A, sTW);
+    constexpr int UP = (ROWS * N + kIpThreads - 1) / kIpThreads;
+    double2 xr[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+        const int it = threadIdx.x + u * kIpThreads;
+        const int r = it / (R + 1), k = it - r * (R + 1);
+        if (r < ROWS) {
+            const double2 zk = A[ipad(r * N + ip_slot<N, 1>(k))];
+            const double2 zc = cconj(A[ipad(r * N + ip_slot<N, 1>(k == 0 ? 0 : N - k))]);
+            const double2 e = make_double2(0.5 * (zk.x + zc.x), 0.5 * (zk.y + zc.y));
+            const double2 d = csub(zk, zc);
+            const double2 o = make_double2(0.5 * d.y, -0.5 * d.x);
+            xr[u] = cadd(e, cmul(__ldg(post + k), o));
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+        const int it = threadIdx.x + u * kIpThreads;
+        const int r = it / (R + 1), k = it - r * (R + 1);
+        if (r < ROWS) A[k * ROWS + (r ^ (k & (ROWS - 1)))] = xr[u];
+    }
+    __syncthreads();
+    const int J = (nlat + 1) / 2;
+    const bool north = i >= nlat - J;
+    const int j = north ? i - (nlat - J) : J - 1 - i;
+    const int h = north ? 0 : 1;
+    const bool equator = north && (J - 1 - j == i);  // odd nlat: G_S := 0 on the equator row
+    const int swz = gt_swz(gl.ntc, j & 7);
+    const long gstep = (long)gl.ns8 * 2 * 8 * gl.sgc;  // doubles between consecutive m
+    const long row0 = (((long)(j >> 3)) * 2 + h) * 8 + (j & 7);
+    const double sc = (1.0 / (2.0 * N)) * roww[i];
+    for (int it = threadIdx.x; it < ROWS * (R + 1); it += kIpThreads) {
+        const int k = it / ROWS, r = it - k * ROWS;
+        if (r >= nrow) continue;
+        const int f = f0 + r, z = f / gl.apg, fl = f - z * gl.apg;
+        const double2 x = A[k * ROWS + (r ^ (k & (ROWS - 1)))];
+        double* p = gtile + ((long)z * (R + 1) + k) * gstep + row0 * gl.sgc + ((2 * fl) ^ swz);
+        *reinterpret_cast<double2*>(p) = make_double2(x.x * sc, x.y * sc);
+        if (equator) *reinterpret_cast<double2*>(p + 8 * gl.sgc) = make_double2(0.0, 0.0);
+    }
+    if (j == J - 1)
+        for (int r = 0; r < nrow; ++r) {
+            const int f = f0 + r, z = f / gl.apg;
+            gt_zero_pad(gtile, gl, R, J, z, h, 2 * (f - z * gl.apg), 2, kIpThreads);
+        }
+}
+
 }  // namespace
+
+// analyse's row transforms into the G tiles of gt_layout_fields(nf) (P.d_gtile); false when
+// nlon/2 has no in-place plan or the tiles do not fit the plan's reservation
+bool fft_r2c_gt(const pswe_plan& P, const double* grid, const GtLayout& gl, int nf, cudaStream_t st) {
+    static const bool off_env = [] { const char* e = getenv("PSWE_FFT_STOCKHAM"); return e && atoi(e) != 0; }();
+    if (off_env || !P.d_gtile || gl.doubles > P.gtile_cap || ip_radix(P.N, 0) == 0) return false;
+    switch (P.N) {
+#define PSWE_CASE(NN)                                                                                     \
+    case NN: {                                                                                            \
+        const size_t sm = (size_t)(8 * ipadded(NN) + ip_ntw(NN, 1)) * sizeof(double2);                  \
+        if (sm > 227 * 1024) return false;                                                                \
+        static bool attr = false;                                                                         \
+        if (!attr) {                                                                                      \
+            PSWE_CUDA(cudaFuncSetAttribute(fft_r2c_gt_kernel<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           227 * 1024));                                                  \
+            attr = true;                                                                                  \
+        }                                                                                                 \
+        fft_r2c_gt_kernel<NN><<<dim3(P.nlat, (nf + 7) / 8), kIpThreads, sm, st>>>(                        \
+            P.R, P.nlat, nf, P.d_fft_iptw1, P.d_fft_post, grid, P.d_gtile, P.d_roww, gl);                 \
+        PSWE_LAUNCH_CHECK();                                                                              \
+        return true;                                                                                      \
+    }
+        PSWE_CASE(24) PSWE_CASE(32) PSWE_CASE(48) PSWE_CASE(64) PSWE_CASE(96) PSWE_CASE(128) PSWE_CASE(192)
+        PSWE_CASE(256) PSWE_CASE(384) PSWE_CASE(512) PSWE_CASE(768) PSWE_CASE(1024)
+#undef PSWE_CASE
+        default: return false;
+    }
+}
 
 bool fft_rows_ip(const pswe_plan& P, bool c2r, const double2* four_in, const double* grid_in, double2* four_out,
                  double* grid_out, int stride, int off, int n, bool cos_flag, int scale_mode, double radius,

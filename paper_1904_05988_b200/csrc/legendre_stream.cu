@@ -453,15 +453,15 @@ __global__ void __launch_bounds__(32 * (W + (PROD ? 1 : 0)), (W == 8 || SUB == 4
     }
     if (!mine) return;
     // C[m = column 8 nt + r4][n = degree-in-parity 2 c4 + v]: t = 16 c + par + 2 (2 c4 + v)
-    const long Kx = (long)(R + 1) * (R + 4) / 2;
-    const long bx = off_ext(R, my_m);
-    const int len = R + 2 - my_m;
-    const int qz = z * 5 * gl.spg;
+    const long Kx = gl.plain ? (long)(R + 1) * (R + 2) / 2 : (long)(R + 1) * (R + 4) / 2;
+    const long bx = gl.plain ? off_std(R, my_m) : off_ext(R, my_m);
+    const int len = R + 2 - my_m - gl.plain;
+    const int qz = z * gl.apg;
 #pragma unroll
     for (int nt = 0; nt < NTC; ++nt) {
         const int col = 8 * nt + r4;
         const int q = qz + (col >> 1);
-        if ((col >> 1) >= 5 * gl.spg || q >= nq) continue;
+        if ((col >> 1) >= gl.apg || q >= nq) continue;
 #pragma unroll
         for (int cc = 0; cc < CPW; ++cc) {
             if (cc >= my_n) continue;
@@ -682,11 +682,11 @@ __global__ void __launch_bounds__(32 * (NTC * H + 1), (NTC * H + 1) <= 8 ? 2 : 1
         if (lane == 0) mbar_arrive(empty + k);
     }
     if (my_n == 0) return;
-    const long Kx = (long)(R + 1) * (R + 4) / 2;
-    const int qz = z * 5 * gl.spg;
+    const long Kx = gl.plain ? (long)(R + 1) * (R + 2) / 2 : (long)(R + 1) * (R + 4) / 2;
+    const int qz = z * gl.apg;
     const int col = 8 * nt + r4;
     const int q = qz + (col >> 1);
-    if ((col >> 1) >= 5 * gl.spg || q >= nq) return;
+    if ((col >> 1) >= gl.apg || q >= nq) return;
 #pragma unroll
     for (int u = 0; u < SPW; ++u) {
         if (u >= my_n) continue;
@@ -694,8 +694,8 @@ __global__ void __launch_bounds__(32 * (NTC * H + 1), (NTC * H + 1) <= 8 ? 2 : 1
         const bool b = slot >= na;
         const int m = b ? ta.w : ta.x;
         const int c = b ? tb.x + (slot - na) : ta.y + slot;
-        const long bx = off_ext(R, m);
-        const int len = R + 2 - m;
+        const long bx = gl.plain ? off_std(R, m) : off_ext(R, m);
+        const int len = R + 2 - m - gl.plain;
 #pragma unroll
         for (int par = 0; par < 2; ++par)
 #pragma unroll
@@ -829,15 +829,15 @@ __global__ void __launch_bounds__(256, 2) leg_fwd_gt_direct_kernel(int R, int Jp
         }
         if (sl + 2 < NSL) load_slice(sl + 2);
     }
-    const long Kx = (long)(R + 1) * (R + 4) / 2;
-    const long bx = off_ext(R, my_m);
-    const int len = R + 2 - my_m;
-    const int qz = z * 5 * gl.spg;
+    const long Kx = gl.plain ? (long)(R + 1) * (R + 2) / 2 : (long)(R + 1) * (R + 4) / 2;
+    const long bx = gl.plain ? off_std(R, my_m) : off_ext(R, my_m);
+    const int len = R + 2 - my_m - gl.plain;
+    const int qz = z * gl.apg;
 #pragma unroll
     for (int nt = 0; nt < NTC; ++nt) {
         const int col = 8 * nt + r4;
         const int q = qz + (col >> 1);
-        if ((col >> 1) >= 5 * gl.spg || q >= nq) continue;
+        if ((col >> 1) >= gl.apg || q >= nq) continue;
 #pragma unroll
         for (int par = 0; par < 2; ++par)
 #pragma unroll
@@ -1367,6 +1367,32 @@ void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t s
         }
     }
 #undef PSWE_FWD_CASES
+}
+
+// analyse on G tiles (gt_layout_fields, written by fft_r2c_gt): the column-warp kernels, the
+// projections' epilogue in the standard coefficient layout. false when no column-warp
+// configuration covers the layout (narrow groups need more than 64 latitude pairs).
+bool analyse_gt_ok(const pswe_plan& P, const GtLayout& gl) {
+    static const bool on = [] {
+        const char* e = getenv("PSWE_ANALYSE_GT");
+        const char* c = getenv("PSWE_FWD_CW");
+        return !(e && atoi(e) == 0) && !(c && atoi(c) == 0) && PSWE_FWD_CW;
+    }();
+    const int nsl = (P.J + 31) / 32;
+    return on && P.legendre_mode == PSWE_LEGENDRE_STREAM && !P.simt && P.n_chunks > 0 && P.d_gtile &&
+           gl.doubles <= P.gtile_cap && (gl.ntc == 4 || (gl.ntc <= 3 && nsl > 2));
+}
+
+void legendre_forward_fields_gt(const pswe_plan& P, const GtLayout& gl, int nf, double2* out, cudaStream_t st) {
+    if (gl.ntc == 4) {
+        fwd_cw_launch<4, 2, 2, 2>(P, gl, nf, out, st);
+    } else if (P.fwd_cfg == 0) {
+        if (gl.ntc == 2) fwd_cw_launch<2, 2, 2, 4>(P, gl, nf, out, st);
+        else fwd_cw_launch<3, 2, 2, 4>(P, gl, nf, out, st);
+    } else {
+        if (gl.ntc == 2) fwd_cw_launch<2, 2, 2, 2>(P, gl, nf, out, st);
+        else fwd_cw_launch<3, 2, 2, 2>(P, gl, nf, out, st);
+    }
 }
 
 // Streamed P table (STREAM mode), built at plan creation; layout in the file header.

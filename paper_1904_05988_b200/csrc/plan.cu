@@ -7,6 +7,7 @@
 //   sectoral seed    legendre.cpp:16-29 (log-space P^m_m, underflows to 0 near the poles)
 //   dealiased_nlon   transform.cpp:38-43
 // Device tables are laid out for the kernels.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <complex>
@@ -150,8 +151,10 @@ void pswe_plan::reserve(int batch) {
             xtile_cap = need;
         }
     }
-    if (n_chunks > 0) {  // G tiles of the eval grid stage; zeroed once: never-written slots stay finite
-        const size_t need = pswe::gt_layout(R, J, batch).doubles;
+    if (n_chunks > 0) {  // G tiles of the eval grid stage (batch states) or of analyse (5 batch
+                         // fields); zeroed once: never-written slots stay finite
+        const size_t need = std::max(pswe::gt_layout(R, J, batch).doubles,
+                                     pswe::gt_layout_fields(R, J, 5 * batch).doubles);
         if (need > gtile_cap) {
             if (d_gtile) cudaFree(d_gtile);
             d_gtile = nullptr;

@@ -171,8 +171,14 @@ namespace pswe {
 // for state b = spg z + b', field f of (Phi'U, Phi'V, qU, qV, ke), the column XOR-swizzled per
 // row by gt_swz (sgc = 8 ntc doubles, no padding; the forward's fragment reads are then
 // conflict-free).
+// Plain analyse (gt_layout_fields): the same tiles with apg single FIELDS per column group (2
+// real columns each, column 2 f' + {re, im} for field f = apg z + f'), and the forward writes
+// the standard coefficient layout out[f K + off_std(m) + s - m] (plain = 1) instead of the
+// extended projections out[q Kx + off_ext(m) + s - m].
 struct GtLayout {
     int spg = 0, groups = 0, ntc = 0, sgc = 0, ns8 = 0;
+    int apg = 0;    // complex arrays (projections / fields) per column group
+    int plain = 0;  // 1: fields in the standard layout (analyse)
     size_t doubles = 0;
 };
 // forward tasks: runs of <= warps x cpw chunks of <= 2 orders m, ~per_sm runs per SM. Two
@@ -189,7 +195,20 @@ inline GtLayout gt_layout(int R, int J, int n) {
     GtLayout g;
     g.spg = n < 5 ? n : 5;
     g.groups = (n + g.spg - 1) / g.spg;
+    g.apg = 5 * g.spg;
     g.ntc = (10 * g.spg + 7) / 8;
+    g.sgc = 8 * g.ntc;
+    g.ns8 = ((J + 31) / 32) * 4;
+    g.doubles = (size_t)g.groups * (R + 1) * g.ns8 * 2 * 8 * g.sgc;
+    return g;
+}
+// nf plain fields: groups of at most 16 fields (4 column tiles), at least 2 column tiles
+inline GtLayout gt_layout_fields(int R, int J, int nf) {
+    GtLayout g;
+    g.groups = (nf + 15) / 16;
+    g.apg = (nf + g.groups - 1) / g.groups;
+    g.ntc = (2 * g.apg + 7) / 8 < 2 ? 2 : (2 * g.apg + 7) / 8;
+    g.plain = 1;
     g.sgc = 8 * g.ntc;
     g.ns8 = ((J + 31) / 32) * 4;
     g.doubles = (size_t)g.groups * (R + 1) * g.ns8 * 2 * 8 * g.sgc;
@@ -249,6 +268,11 @@ void fft_eval_products(const pswe_plan& P, const pswe_params& prm, const double2
 bool gt_path_ok(const pswe_plan& P, int n);
 void fft_eval_products_gt(const pswe_plan& P, const pswe_params& prm, const double2* fin, int n, cudaStream_t st);
 void legendre_forward_gt(const pswe_plan& P, int n, double2* out, cudaStream_t st);
+// analyse on G tiles: fft_r2c_gt writes the nf fields' tiles (gt_layout_fields), the column-warp
+// forward writes the coefficients (standard layout); analyse_gt_ok: the pair applies
+bool analyse_gt_ok(const pswe_plan& P, const GtLayout& gl);
+bool fft_r2c_gt(const pswe_plan& P, const double* grid, const GtLayout& gl, int nf, cudaStream_t st);
+void legendre_forward_fields_gt(const pswe_plan& P, const GtLayout& gl, int nf, double2* out, cudaStream_t st);
 // fft_ip.cu: in-place fused grid stage; false if nlon/2 has no in-place plan
 std::vector<double2> fft_ip_twiddles(int N, int pl = 0);
 bool fft_eval_products_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, double2* fout, int n,
