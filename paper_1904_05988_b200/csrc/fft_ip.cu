@@ -262,7 +262,9 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N, PL))
     }
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
+#ifndef PSWE_FDIAG_NOFFT
     DifGuard<N, 0, 4, true, PL>::run(A, sTW);
+#endif
 
     // grid-point products (swe.cpp:41-54), two grid points per complex slot, slot order permuted
     const double c = rowc[i];
@@ -289,7 +291,9 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N, PL))
         for (int q = 0; q < 5; ++q) A[q * RS + p] = make_double2(o[q][0], o[q][1]);
     }
     __syncthreads();
+#ifndef PSWE_FDIAG_NOFFT
     DitGuard<N, ip_npass(N, PL) - 1, 5, false, PL>::run(A, sTW);
+#endif
 
     const double nl = 2.0 * N;
     const double sflux = (1.0 / nl) * (inv_a * roww[i] / (c * c));
