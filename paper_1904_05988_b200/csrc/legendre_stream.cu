@@ -975,6 +975,9 @@ __global__ void __launch_bounds__(CH * kPrepItems)
 #ifndef PSWE_PREP_ROWS
 #define PSWE_PREP_ROWS 1
 #endif
+#ifndef PSWE_PREP_PLAIN
+#define PSWE_PREP_PLAIN 1
+#endif
 constexpr int kPrepRowChunks = 8;
 template <int NT>
 __global__ void __launch_bounds__(CH * kPrepRowChunks)
@@ -1044,6 +1047,57 @@ __global__ void __launch_bounds__(CH * kPrepRowChunks)
     const int nv = nchk * TILE / 4;
     for (int i = threadIdx.x; i < nv; i += CH * kPrepRowChunks) {
         const double4 w = src[i];
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(dst + 4 * i), "d"(w.x), "d"(w.y), "d"(w.z),
+                     "d"(w.w)
+                     : "memory");
+    }
+}
+
+// synthesise's prep (PLAIN, standard layout): one thread per (chunk, degree) writes that degree's
+// whole X-tile row of column group z = blockIdx.y - the 4 NT fields' coefficients, issued as one
+// batch of loads (the generic kernel's one load per thread left too few bytes in flight: 8 us for
+// 16 MB), the pad columns zero - staged in shared memory and stored as 32-byte vectors like
+// xtile_prep_rows_kernel.
+template <int NT>
+__global__ void __launch_bounds__(CH * kPrepRowChunks)
+    xtile_prep_plain_kernel(int R, int nq, int nct, const int* __restrict__ chunk_desc,
+                            const double2* __restrict__ in, double* __restrict__ Xt) {
+    constexpr int SX = 8 * NT + 2;
+    constexpr int TILE = CH * SX;
+    __shared__ __align__(32) double sx[kPrepRowChunks * TILE];
+    const int cg0 = blockIdx.x * kPrepRowChunks;
+    const int cg = cg0 + threadIdx.x / CH;
+    const int tl = threadIdx.x % CH;
+    const int z = blockIdx.y;
+    const int nchk = min(kPrepRowChunks, nct - cg0);
+    pdl_trigger();
+    if (cg < nct) {
+        const int2 mc = reinterpret_cast<const int2*>(chunk_desc)[cg];  // (m, chunk within m)
+        const int m = mc.x;
+        const int t = mc.y * CH + tl;
+        const long K = (long)(R + 1) * (R + 2) / 2;
+        const double2* src = in + off_std(R, m) + t;
+        const bool live = m + t <= R;
+        pdl_wait();  // the coefficients may come from the preceding kernel
+        double2 v[4 * NT];
+#pragma unroll
+        for (int f = 0; f < 4 * NT; ++f) {
+            const int q = z * 4 * NT + f;
+            v[f] = live && q < nq ? src[(long)q * K] : make_double2(0.0, 0.0);
+        }
+        double2* row = reinterpret_cast<double2*>(sx + (threadIdx.x / CH) * TILE + tl * SX);
+#pragma unroll
+        for (int f = 0; f < 4 * NT; ++f) row[f] = v[f];
+        row[4 * NT] = make_double2(0.0, 0.0);  // pad columns
+    } else {
+        pdl_wait();
+    }
+    __syncthreads();
+    const double4* s4 = reinterpret_cast<const double4*>(sx);
+    double* dst = Xt + ((long)z * nct + cg0) * TILE;  // 32-byte aligned: cg0 % 8 == 0, TILE even
+    const int nv = nchk * TILE / 4;
+    for (int i = threadIdx.x; i < nv; i += CH * kPrepRowChunks) {
+        const double4 w = s4[i];
         asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(dst + 4 * i), "d"(w.x), "d"(w.y), "d"(w.z),
                      "d"(w.w)
                      : "memory");
@@ -1582,7 +1636,18 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
     else if (kind == INV_UV)
         launch_pdl(xtile_prep_kernel<INV_UV>, g, dim3(CH * ipb), 0, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m,
                    P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
-    else
+    else if (PSWE_PREP_PLAIN) {
+        const dim3 gp((P.n_chunks + kPrepRowChunks - 1) / kPrepRowChunks, groups);
+        switch (NT) {
+#define PSWE_PREP_CASE(T)                                                                                    \
+    case T:                                                                                              \
+        launch_pdl(xtile_prep_plain_kernel<T>, gp, dim3(CH * kPrepRowChunks), 0, st, P.R, nq, P.n_chunks, \
+                   P.d_chunk_m, in, P.d_xtile);                                                           \
+        break;
+            PSWE_PREP_CASE(1) PSWE_PREP_CASE(2) PSWE_PREP_CASE(3) PSWE_PREP_CASE(4) PSWE_PREP_CASE(5)
+#undef PSWE_PREP_CASE
+        }
+    } else
         launch_pdl(xtile_prep_kernel<INV_PLAIN>, g, dim3(CH * ipb), 0, st, P.R, NQ, SX, nq, P.n_chunks, P.d_chunk_m,
                    P.d_eps, P.d_rlap, in, in2, radius, P.d_xtile);
     PSWE_LAUNCH_CHECK();

@@ -72,6 +72,27 @@ def test_sweep_matches_oracle_sweep(P):
     assert abs(r - rr) <= 1e-6 * rr + 64 * 2**-52 * np.abs(th[0]).max()
 
 
+@pytest.mark.parametrize("nodes,R", [(2, 15), (3, 31), (5, 63)])
+def test_fused_tail_residual_bit_identical(P, nodes, R):
+    """sdc_step's last sweep ends in one kernel that finishes the last node's evaluation and
+    computes the collocation residual (tail_residual_kernel); the separate residual kernel over the
+    stored right-hand sides must give the same bits, and the stored F[M] must be the separate
+    tail's (a second step from the same state reproduces every node bit for bit)."""
+    prm = P.ModelParams(phi_bar=PHI_BAR, nu=1e5)
+    lvl = P.Level(P.TransformPlan(R), prm, nodes)
+    th = cuda(fx.smooth_state(R, PHI_BAR, 5))
+    r_fused = torch.zeros(1, dtype=torch.float64, device="cuda")
+    lvl.sdc_step(th, 90.0, 2, r_fused)
+    r_sep = lvl.collocation_residual(90.0)
+    torch.cuda.synchronize()
+    assert host(r_fused)[0] == host(r_sep)[0] and host(r_sep)[0] > 0
+    first = [host(lvl.f_exp(m)).copy() for m in range(nodes)] + [host(lvl.f_imp(m)).copy() for m in range(nodes)]
+    lvl.sdc_step(th, 90.0, 2, None)  # the last sweep's tail by the separate kernel
+    again = [host(lvl.f_exp(m)) for m in range(nodes)] + [host(lvl.f_imp(m)) for m in range(nodes)]
+    for a, b in zip(first, again):
+        assert np.array_equal(a, b)
+
+
 def _pair(P, mode=0):
     p = P.ModelParams(phi_bar=PHI_BAR)
     pf, pc = P.TransformPlan(31, 0, 0, mode), P.TransformPlan(15, 0, 0, mode)
