@@ -978,6 +978,9 @@ __global__ void __launch_bounds__(CH * kPrepItems)
 #ifndef PSWE_PREP_PLAIN
 #define PSWE_PREP_PLAIN 1
 #endif
+#ifndef PSWE_PREP_WIDE
+#define PSWE_PREP_WIDE 1
+#endif
 constexpr int kPrepRowChunks = 8;
 template <int NT>
 __global__ void __launch_bounds__(CH * kPrepRowChunks)
@@ -1047,6 +1050,72 @@ __global__ void __launch_bounds__(CH * kPrepRowChunks)
     const int nv = nchk * TILE / 4;
     for (int i = threadIdx.x; i < nv; i += CH * kPrepRowChunks) {
         const double4 w = src[i];
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(dst + 4 * i), "d"(w.x), "d"(w.y), "d"(w.z),
+                     "d"(w.w)
+                     : "memory");
+    }
+}
+
+// The evaluation's prep for wide column groups (NT >= 3 states, the batch): thread (degree tl,
+// state ql, chunk) computes its state's four columns with the same expressions as
+// xtile_prep_rows_kernel (xrow.cuh), so each thread keeps one state's 7 loads in flight at 64
+// registers instead of NT states' at 178; the block's kPrepWideChunks tiles are staged in shared
+// memory and stored as 32-byte vectors (the generic kernel's 16-byte row stores at a 16 SX-byte
+// stride: 80-thread blocks, long_scoreboard 46%, drain/lg_throttle 14%).
+constexpr int kPrepWideChunks = 4;
+template <int NT>
+__global__ void __launch_bounds__(CH * NT * kPrepWideChunks)
+    xtile_prep_wide_kernel(int R, int n, int nct, const int* __restrict__ chunk_desc, const double* __restrict__ eps,
+                           const double* __restrict__ rtab, const double2* __restrict__ in, double radius,
+                           double* __restrict__ Xt) {
+    constexpr int SX = 8 * NT + 2;
+    constexpr int TILE = CH * SX;
+    constexpr int NTH = CH * NT * kPrepWideChunks;
+    __shared__ __align__(32) double sx[kPrepWideChunks * TILE];
+    const int tl = threadIdx.x % CH;
+    const int ql = (threadIdx.x / CH) % NT;
+    const int cb = threadIdx.x / (CH * NT);
+    const int cg0 = blockIdx.x * kPrepWideChunks;
+    const int cg = cg0 + cb;
+    const int z = blockIdx.y;
+    const int nchk = min(kPrepWideChunks, nct - cg0);
+    pdl_trigger();
+    if (cg < nct) {
+        const int2 mc = reinterpret_cast<const int2*>(chunk_desc)[cg];  // (m, chunk within m)
+        const int m = mc.x;
+        const int t = mc.y * CH + tl;
+        const int s = m + t;
+        const long K = (long)(R + 1) * (R + 2) / 2;
+        const long bs = off_std(R, m), bx = off_ext(R, m);
+        const int sm1 = max(s - 1, m), sp1 = min(s + 1, R), s0 = min(s, R);
+        const int item = z * NT + ql;
+        const bool live = s <= R + 1 && item < n;
+        xrow::Fac F{};
+        if (live) F = xrow::factors(R, m, s, bx, eps, rtab, radius);
+        pdl_wait();  // the states come from the preceding kernel
+        double2 v[4];
+        if (live) {
+            const double2* st = in + (long)item * 3 * K + bs - m;
+            const double2 ph = st[s0], vm = st[K + sm1], v0 = st[K + s0], vp = st[K + sp1];
+            const double2 dm = st[2 * K + sm1], d0 = st[2 * K + s0], dp = st[2 * K + sp1];
+            xrow::columns(F, R, m, s, radius, ph, vm, v0, vp, dm, d0, dp, v);
+        } else {
+#pragma unroll
+            for (int f = 0; f < 4; ++f) v[f] = make_double2(0.0, 0.0);
+        }
+        double2* row = reinterpret_cast<double2*>(sx + cb * TILE + tl * SX);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) row[4 * ql + f] = v[f];
+        if (ql == 0) row[4 * NT] = make_double2(0.0, 0.0);  // pad columns
+    } else {
+        pdl_wait();
+    }
+    __syncthreads();
+    const double4* s4 = reinterpret_cast<const double4*>(sx);
+    double* dst = Xt + ((long)z * nct + cg0) * TILE;  // 32-byte aligned: cg0 % 4 == 0, TILE even
+    const int nv = nchk * TILE / 4;
+    for (int i = threadIdx.x; i < nv; i += NTH) {
+        const double4 w = s4[i];
         asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};\n" ::"l"(dst + 4 * i), "d"(w.x), "d"(w.y), "d"(w.z),
                      "d"(w.w)
                      : "memory");
@@ -1628,6 +1697,20 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
                    P.d_eps, P.d_rlap, in, radius, P.d_xtile);                                                  \
         break;
             PSWE_PREP_CASE(1) PSWE_PREP_CASE(2) PSWE_PREP_CASE(3) PSWE_PREP_CASE(4) PSWE_PREP_CASE(5)
+#undef PSWE_PREP_CASE
+        }
+    } else if (kind == INV_EVAL && PSWE_PREP_WIDE && NT >= 3 && P.R <= 255) {
+        // (measured r2bd: T255 5-state prep 12.5 -> 11.2 us, batch 95.2 -> 94.2 us, bit-identical over
+        // eval_dump's 50 cases; at T511 the generic kernel's small blocks stay faster, 23.3 vs 25 us)
+        const dim3 gw((P.n_chunks + kPrepWideChunks - 1) / kPrepWideChunks, groups);
+        const int n = nq / 4;
+        switch (NT) {
+#define PSWE_PREP_CASE(T)                                                                                      \
+    case T:                                                                                                \
+        launch_pdl(xtile_prep_wide_kernel<T>, gw, dim3(CH * T * kPrepWideChunks), 0, st, P.R, n, P.n_chunks, \
+                   P.d_chunk_m, P.d_eps, P.d_rlap, in, radius, P.d_xtile);                                  \
+        break;
+            PSWE_PREP_CASE(3) PSWE_PREP_CASE(4) PSWE_PREP_CASE(5)
 #undef PSWE_PREP_CASE
         }
     } else if (kind == INV_EVAL)
