@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-pfasst", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sizes", action="store_true", help="skip the T511/T1023 Legendre roofline lines")
     ap.add_argument("--legendre", type=int, default=1, help="0 recompute, 1 stream (default, measured faster)")
     return ap.parse_args()
 
@@ -409,6 +410,37 @@ def run_ours(args):
                           "ncu --set full, cache flushed)",
         "kernels": stages,
     }
+
+    # the same kernels on the larger BASELINE grids (configs 4/5): the Legendre contractions'
+    # fraction of the FP64 peak once the problem fills the GPU (one wave at T255, several beyond)
+    by_size = {}
+    if not args.no_sizes:
+        for Rs, nls, nlo in ((511, 512, 1024), (1023, 1024, 2048)):
+            try:
+                splan = P.TransformPlan(Rs, nls, nlo, args.legendre)
+                splan.reserve(BATCH)
+                sst = torch.as_tensor(bench_states(Rs)).to(dev)
+                sfi, sfe = torch.empty_like(sst), torch.empty_like(sst)
+                acc5, reps = np.zeros(5), 5
+                for k in range(reps + 1):
+                    flush.zero_()
+                    _lib.check(L.pswe_eval_imex_kernel_times(splan.handle, ctypes.byref(cprm), sst.data_ptr(),
+                                                             sfi.data_ptr(), sfe.data_ptr(), BATCH, _stream(), ms5))
+                    if k:
+                        acc5 += np.array(list(ms5))
+                acc5 /= reps
+                FLs = nls * (Rs + 1) * (Rs + 2)
+                ent = {"workload": f"rhs_eval T{Rs} {nls}x{nlo} x{BATCH} states", "stage_ms": dict(zip(names, acc5.tolist()))}
+                for n, nf, col in (("legendre_inverse", 4, 1), ("legendre_forward", 5, 3)):
+                    tf = nf * BATCH * FLs / (acc5[col] * 1e-3) / 1e12
+                    ent[n] = {"ms": float(acc5[col]), "achieved": tf, "peak": peak_fp64, "unit": "TFLOP/s",
+                              "frac": tf / peak_fp64}
+                by_size[f"T{Rs}"] = ent
+                del splan, sst, sfi, sfe
+            except Exception as e:  # reported, never hides the headline
+                by_size[f"T{Rs}"] = {"error": f"{type(e).__name__}: {e}"}
+        torch.cuda.empty_cache()
+    roofline["by_size"] = by_size
 
     # e2e through the public C ABI (pswe_eval_imex, the drop-in boundary) with pinned host
     # buffers: every step copies its 5 input states host -> device, evaluates, and copies both
