@@ -220,6 +220,12 @@ int pswe_pfasst_run_block(pswe_pfasst* pf, const double* theta0, double* final_s
  * states, may be NULL) receives the fine last-node state of every time step of the block. */
 int pswe_pfasst_run_block_steps(pswe_pfasst* pf, const double* theta0, double* step_final, double* final_state,
                                 double* residuals, void* stream);
+/* n_blocks blocks chained as the reference's runner does (runner.cpp:145-151): block b starts from
+ * block b-1's final state. final_state (device) receives the last block's; residuals_dev (device,
+ * may be NULL) n_blocks * n_time_steps * (n_iter+1) doubles, block-major. Serial emulation runs
+ * without any host synchronisation (read the results after synchronising the stream). */
+int pswe_pfasst_run_blocks(pswe_pfasst* pf, const double* theta0, int n_blocks, double* final_state,
+                           double* residuals_dev, void* stream);
 /* Message log of the last block (pfasst.hpp:22-31), 7 ints per record:
  * phase, iteration, step ('B','P','A','C'), sender, receiver, level, node. Returns the count. */
 int pswe_pfasst_messages(const pswe_pfasst* pf, int* out, int max_records);

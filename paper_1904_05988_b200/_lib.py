@@ -84,6 +84,7 @@ SIGNATURES = {
     "pswe_pfasst_run_block_steps": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "pswe_pfasst_destroy": (_i, [_vp]),
     "pswe_pfasst_run_block": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "pswe_pfasst_run_blocks": (_i, [_vp, _vp, _i, _vp, _vp, _vp]),
     "pswe_pfasst_messages": (_i, [_vp, _pi, _i]),
     "pswe_pfasst_schedule": (_i, [_i, _i, _i, _pi, _i]),
     "pswe_pfasst_schedule_ml": (_i, [_i, _i, _i, _i, _pi, _i]),

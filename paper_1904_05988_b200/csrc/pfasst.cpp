@@ -746,6 +746,73 @@ int pswe_pfasst_destroy(pswe_pfasst* pf) {
     });
 }
 
+// One serial-emulation block on stream st: theta0 -> pf->d_res (residuals, device), final_state /
+// step_final (device, optional). No host synchronisation. final_state may alias theta0 (theta0 is
+// consumed before final_state is written: graph path copies it first, eager path reads it during
+// the block and final_state is written last).
+static void serial_block(pswe_pfasst* pf, const double2* th, double* step_final, double* final_state,
+                         cudaStream_t st) {
+    const int n = pf->cfg.n_time_steps, N = pf->cfg.n_iter;
+    PSWE_CUDA(cudaMemsetAsync(pf->d_res, 0, sizeof(double) * n * (N + 1), st));
+    if (!pf->use_graph) {
+        run_serial(pf, th, st);
+    } else {
+        // the block is a fixed sequence of ~10^2-10^3 small launches: capture it once and
+        // replay it (no host launch overhead, no host logic per kernel)
+        // capture/launch on an internal stream (the caller's may be the legacy default
+        // stream, which cannot be captured), ordered after / before the caller's stream
+        if (!pf->d_theta) {
+            PSWE_CUDA(cudaMalloc(&pf->d_theta, state_bytes(pf->Kf)));
+            PSWE_CUDA(cudaStreamCreateWithFlags(&pf->gstream, cudaStreamNonBlocking));
+            PSWE_CUDA(cudaEventCreateWithFlags(&pf->ev_in, cudaEventDisableTiming));
+            PSWE_CUDA(cudaEventCreateWithFlags(&pf->ev_out, cudaEventDisableTiming));
+        }
+        const cudaStream_t gs = pf->gstream;
+        // the graph holds raw pointers into the levels' plan scratch, which is grow-only
+        // and reallocated by a larger eval/transform batch, pswe_plan_reserve or a level
+        // with more nodes: any change since the capture makes it stale -> run eagerly once
+        // (re-sizing every pool), then capture again
+        const unsigned long long gen = plans_generation(pf);
+        if (pf->graph && gen != pf->graph_gen) {
+            PSWE_CUDA(cudaGraphExecDestroy(pf->graph));
+            pf->graph = nullptr;
+            pf->eager_runs = 0;
+        }
+        PSWE_CUDA(cudaMemcpyAsync(pf->d_theta, th, state_bytes(pf->Kf), cudaMemcpyDeviceToDevice, st));
+        PSWE_CUDA(cudaEventRecord(pf->ev_in, st));
+        PSWE_CUDA(cudaStreamWaitEvent(gs, pf->ev_in, 0));
+        if (!pf->graph && pf->eager_runs >= 1) {
+            cudaGraph_t g = nullptr;
+            PSWE_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+            try {
+                run_serial(pf, pf->d_theta, gs);
+            } catch (...) {
+                cudaStreamEndCapture(gs, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            PSWE_CUDA(cudaStreamEndCapture(gs, &g));
+            PSWE_CUDA(cudaGraphInstantiate(&pf->graph, g, 0));
+            cudaGraphDestroy(g);
+            pf->graph_gen = plans_generation(pf);
+        }
+        if (pf->graph) {
+            PSWE_CUDA(cudaGraphLaunch(pf->graph, gs));
+        } else {
+            run_serial(pf, pf->d_theta, gs);
+            ++pf->eager_runs;
+        }
+        PSWE_CUDA(cudaEventRecord(pf->ev_out, gs));
+        PSWE_CUDA(cudaStreamWaitEvent(st, pf->ev_out, 0));
+    }
+    if (final_state)
+        PSWE_CUDA(cudaMemcpyAsync(final_state, st_ptr(pf->fine, pf->mf - 1), state_bytes(pf->Kf),
+                                  cudaMemcpyDeviceToDevice, st));
+    if (step_final)
+        PSWE_CUDA(cudaMemcpyAsync(step_final, pf->d_step_final, n * state_bytes(pf->Kf),
+                                  cudaMemcpyDeviceToDevice, st));
+}
+
 int pswe_pfasst_run_block_steps(pswe_pfasst* pf, const double* theta0, double* step_final, double* final_state,
                                 double* residuals, void* stream) {
     return guarded([&] {
@@ -755,70 +822,14 @@ int pswe_pfasst_run_block_steps(pswe_pfasst* pf, const double* theta0, double* s
         const cudaStream_t st = as_stream(stream);
         const double2* th = reinterpret_cast<const double2*>(theta0);
         const int n = pf->cfg.n_time_steps, N = pf->cfg.n_iter;
-        PSWE_CUDA(cudaMemsetAsync(pf->d_res, 0, sizeof(double) * n * (N + 1), st));
         if (!pf->distributed) {
-            if (!pf->use_graph) {
-                run_serial(pf, th, st);
-            } else {
-                // the block is a fixed sequence of ~10^2-10^3 small launches: capture it once and
-                // replay it (no host launch overhead, no host logic per kernel)
-                // capture/launch on an internal stream (the caller's may be the legacy default
-                // stream, which cannot be captured), ordered after / before the caller's stream
-                if (!pf->d_theta) {
-                    PSWE_CUDA(cudaMalloc(&pf->d_theta, state_bytes(pf->Kf)));
-                    PSWE_CUDA(cudaStreamCreateWithFlags(&pf->gstream, cudaStreamNonBlocking));
-                    PSWE_CUDA(cudaEventCreateWithFlags(&pf->ev_in, cudaEventDisableTiming));
-                    PSWE_CUDA(cudaEventCreateWithFlags(&pf->ev_out, cudaEventDisableTiming));
-                }
-                const cudaStream_t gs = pf->gstream;
-                // the graph holds raw pointers into the levels' plan scratch, which is grow-only
-                // and reallocated by a larger eval/transform batch, pswe_plan_reserve or a level
-                // with more nodes: any change since the capture makes it stale -> run eagerly once
-                // (re-sizing every pool), then capture again
-                const unsigned long long gen = plans_generation(pf);
-                if (pf->graph && gen != pf->graph_gen) {
-                    PSWE_CUDA(cudaGraphExecDestroy(pf->graph));
-                    pf->graph = nullptr;
-                    pf->eager_runs = 0;
-                }
-                PSWE_CUDA(cudaMemcpyAsync(pf->d_theta, th, state_bytes(pf->Kf), cudaMemcpyDeviceToDevice, st));
-                PSWE_CUDA(cudaEventRecord(pf->ev_in, st));
-                PSWE_CUDA(cudaStreamWaitEvent(gs, pf->ev_in, 0));
-                if (!pf->graph && pf->eager_runs >= 1) {
-                    cudaGraph_t g = nullptr;
-                    PSWE_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
-                    try {
-                        run_serial(pf, pf->d_theta, gs);
-                    } catch (...) {
-                        cudaStreamEndCapture(gs, &g);
-                        if (g) cudaGraphDestroy(g);
-                        throw;
-                    }
-                    PSWE_CUDA(cudaStreamEndCapture(gs, &g));
-                    PSWE_CUDA(cudaGraphInstantiate(&pf->graph, g, 0));
-                    cudaGraphDestroy(g);
-                    pf->graph_gen = plans_generation(pf);
-                }
-                if (pf->graph) {
-                    PSWE_CUDA(cudaGraphLaunch(pf->graph, gs));
-                } else {
-                    run_serial(pf, pf->d_theta, gs);
-                    ++pf->eager_runs;
-                }
-                PSWE_CUDA(cudaEventRecord(pf->ev_out, gs));
-                PSWE_CUDA(cudaStreamWaitEvent(st, pf->ev_out, 0));
-            }
-            if (final_state)
-                PSWE_CUDA(cudaMemcpyAsync(final_state, st_ptr(pf->fine, pf->mf - 1), state_bytes(pf->Kf),
-                                          cudaMemcpyDeviceToDevice, st));
-            if (step_final)
-                PSWE_CUDA(cudaMemcpyAsync(step_final, pf->d_step_final, n * state_bytes(pf->Kf),
-                                          cudaMemcpyDeviceToDevice, st));
+            serial_block(pf, th, step_final, final_state, st);
             if (residuals) {
                 PSWE_CUDA(cudaMemcpyAsync(residuals, pf->d_res, sizeof(double) * n * (N + 1), cudaMemcpyDeviceToHost, st));
                 PSWE_CUDA(cudaStreamSynchronize(st));
             }
         } else {
+            PSWE_CUDA(cudaMemsetAsync(pf->d_res, 0, sizeof(double) * n * (N + 1), st));
             // BlockResult: the last step's final state goes to every rank (next block's theta0,
             // runner.cpp:145-147), step_final (optional) gathers every rank's, residual rows are
             // gathered everywhere; end_block bounds every wait by the receive timeout
@@ -868,6 +879,39 @@ int pswe_pfasst_run_block_steps(pswe_pfasst* pf, const double* theta0, double* s
                 throw;
             }
             if (residuals) std::memcpy(residuals, all.data(), sizeof(double) * all.size());
+        }
+    });
+}
+
+// runner.cpp:145-151: n_blocks blocks chained (block b's theta0 = block b-1's final state). Serial
+// emulation: everything is enqueued on the stream without a host synchronisation; residuals
+// (device, n_blocks * n_time_steps * (n_iter+1)) are valid once the stream has been synchronised.
+// Distributed: one host-synchronising block at a time (the block end gathers over the ranks).
+int pswe_pfasst_run_blocks(pswe_pfasst* pf, const double* theta0, int n_blocks, double* final_state,
+                           double* residuals_dev, void* stream) {
+    return guarded([&] {
+        PSWE_NVTX("pswe.pfasst.run_blocks");
+        if (!pf || !theta0 || !final_state || n_blocks < 0) throw std::invalid_argument("NULL argument");
+        if (pf->broken) throw std::runtime_error("pfasst: a previous block failed; destroy and recreate the controller");
+        const cudaStream_t st = as_stream(stream);
+        const int n = pf->cfg.n_time_steps, N = pf->cfg.n_iter;
+        const size_t rb = sizeof(double) * n * (N + 1);
+        const double* th = theta0;
+        std::vector<double> host(pf->distributed ? (size_t)n * (N + 1) : 0);
+        for (int b = 0; b < n_blocks; ++b) {
+            if (!pf->distributed) {
+                serial_block(pf, reinterpret_cast<const double2*>(th), nullptr, final_state, st);
+                if (residuals_dev)
+                    PSWE_CUDA(cudaMemcpyAsync(residuals_dev + (size_t)b * n * (N + 1), pf->d_res, rb,
+                                              cudaMemcpyDeviceToDevice, st));
+            } else {
+                if (pswe_pfasst_run_block_steps(pf, th, nullptr, final_state, host.data(), stream))
+                    throw std::runtime_error(pswe_last_error());
+                if (residuals_dev)
+                    PSWE_CUDA(cudaMemcpy(residuals_dev + (size_t)b * n * (N + 1), host.data(), rb,
+                                         cudaMemcpyHostToDevice));
+            }
+            th = final_state;
         }
     });
 }
