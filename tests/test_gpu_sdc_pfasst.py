@@ -134,6 +134,28 @@ def test_pfasst_serial_emulation(P, golden, n_ts, n_blocks, mode):
     assert mine == ref_log
 
 
+@pytest.mark.parametrize("n_ts", [1, 2])
+def test_run_blocks_matches_block_by_block(P, golden, n_ts):
+    """pswe_pfasst_run_blocks (runner.cpp:145-151, no host synchronisation between blocks) against
+    the same blocks run one call at a time with the host read-back: bit-identical final state and
+    residual history; n_blocks = 0 leaves theta0 as the result."""
+    th = cuda(golden["pf_theta0"])
+    pair, _ = _pair(P)
+    pf = P.Pfasst(pair, P.BlockConfig(n_ts, 60.0, 3))
+    fin, hist = P.run_blocks(pf, th, 3)
+    s, rows = th.clone(), []
+    for _ in range(3):
+        f1, r1 = pf.run_block(s)
+        s.copy_(f1)
+        rows.append(r1)
+    np.testing.assert_array_equal(host(fin), host(s))
+    np.testing.assert_array_equal(hist, np.array(rows))
+    fin0, hist0 = P.run_blocks(pf, th, 0)
+    np.testing.assert_array_equal(host(fin0), host(th))
+    assert hist0.shape == (0, n_ts, 4)
+    pf.close()
+
+
 def test_pfasst_nccl_executor_single_rank(P, golden):
     """The NCCL executor on one GPU (world = 1): communicator set-up, the final-state broadcast and
     the residual all-gather; the result must equal the serial-emulation / reference run."""
