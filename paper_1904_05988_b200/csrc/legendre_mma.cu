@@ -403,7 +403,7 @@ void build_legendre_checkpoints(pswe_plan& P) {
 // n=1: 330 vs 383 us). PSWE_STREAM_INV_MAX_J overrides the size threshold (tuning only).
 bool use_stream_inverse(const pswe_plan& P, int nq) {
     static const int maxj = [] { const char* e = std::getenv("PSWE_STREAM_INV_MAX_J"); return e ? std::atoi(e) : 384; }();
-    return P.legendre_mode == PSWE_LEGENDRE_STREAM && (P.J <= maxj || nq > 4);
+    return P.legendre_mode == PSWE_LEGENDRE_STREAM && (P.J <= maxj || nq > 4 || inv_rec_big(P, nq));
 }
 
 // Inverse Legendre on DMMA. nq complex columns: PLAIN = fields, UV = 2 per pair, EVAL = 4 per state.

@@ -1666,7 +1666,8 @@ bool xtiles_by_sweep_ok(const pswe_plan& P) {
     return !P.simt && use_stream_inverse(P, 4) && inv_choose_nt(P, 4, INV_EVAL) == 1;
 }
 void legendre_inverse_prepared(const pswe_plan& P, double2* out, cudaStream_t st) {
-    inv_tma_launch<1>(P, P.d_xtile, 4, out, st);
+    if (inv_rec_big(P, 4)) inv_rec_launch(P, P.d_xtile, 4, 1, out, st);
+    else inv_tma_launch<1>(P, P.d_xtile, 4, out, st);
 }
 
 // kind/nq/in/in2/radius as legendre_inverse_mma: tiled prep, then the TMA-pipelined contraction.
@@ -1738,6 +1739,10 @@ void legendre_inverse_stream(const pswe_plan& P, int kind, const double2* in, co
 #ifdef PSWE_DIAG_NOINV
     return;
 #endif
+    if (inv_rec_big(P, nq)) {
+        inv_rec_launch(P, P.d_xtile, nq, NT, out, st);
+        return;
+    }
     switch (NT) {
         case 5: inv_tma_launch<5>(P, P.d_xtile, nq, out, st); break;
         case 4: inv_tma_launch<4>(P, P.d_xtile, nq, out, st); break;

@@ -241,6 +241,9 @@ bool use_stream_inverse(const pswe_plan& P, int nq);
 void xtile_reserve(const pswe_plan& P, int nq, int kind);
 bool xtiles_by_sweep_ok(const pswe_plan& P);
 void legendre_inverse_prepared(const pswe_plan& P, double2* out, cudaStream_t st);
+// legendre_rec.cu: single-state inverse on large grids on the CUDA cores, P recomputed in registers
+bool inv_rec_big(const pswe_plan& P, int nq);
+void inv_rec_launch(const pswe_plan& P, const double* Xt, int nq, int NT, double2* out, cudaStream_t st);
 // capi.cu: an evaluation up to the five projections in P.d_proj
 void eval_imex_proj(pswe_plan& P, const pswe_params& prm, const double2* state, int n, cudaStream_t st,
                     bool xprep = false);
