@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N, PL))
     double* gt = nullptr;
     long gstep = 0;
     int swz = 0, gcol = 0;
-    bool equator = false;
+    bool equator = false, last_state = false;
     if constexpr (GT) {
         const int J = (nlat + 1) / 2;
         const bool north = i >= nlat - J;
@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N, PL))
         gstep = (long)gl.ns8 * 2 * 8 * gl.sgc;  // doubles between consecutive m
         swz = gt_swz(gl.ntc, j & 7);
         gcol = 10 * bl;
+        last_state = bl == min(gl.spg, (int)gridDim.y - z * gl.spg) - 1;
     }
     for (int k = threadIdx.x; k <= R; k += kIpThreads) {
         const double2 w = __ldg(post + k);
@@ -356,7 +357,12 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N, PL))
             if ((gcol & 3) == 0) {
                 st4(gcol, v[0], v[1], v[2], v[3]);
                 st4(gcol + 4, v[4], v[5], v[6], v[7]);
-                st2(gcol + 8, v[8], v[9]);
+                // the group's last state ends mid-sector: its padding half (two columns the forward
+                // multiplies but never stores) is written with zeros, so every 32-byte sector of the
+                // tile row is written whole (a partially written sector costs a DRAM read-modify-
+                // write once the tiles outgrow the L2: T1023 single state, 134 MB of tiles)
+                if (last_state && gcol + 12 <= gl.sgc) st4(gcol + 8, v[8], v[9], 0.0, 0.0);
+                else st2(gcol + 8, v[8], v[9]);
             } else {
                 st2(gcol, v[0], v[1]);
                 st4(gcol + 2, v[2], v[3], v[4], v[5]);
