@@ -216,7 +216,10 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N, PL))
                        GtLayout gl) {
     extern __shared__ double2 A[];  // [5][N], ipad layout; then the twiddles [ip_ntw(N)]
     double2* sTW = A + 5 * ipadded(N);
-    const int i = blockIdx.x, b = blockIdx.y;
+    // GT: the states of one latitude row are consecutive blocks (grid (n, nlat)), so the G-tile
+    // sectors two states share are written close together in time (merged in L2 instead of
+    // read-modify-written in DRAM when the tiles outgrow it: T1023 with several states)
+    const int i = GT ? blockIdx.y : blockIdx.x, b = GT ? blockIdx.x : blockIdx.y;
     // twiddles to shared memory (cp.async, overlapped with the row loads; waited before the
     // first barrier)
     for (int t = threadIdx.x; t < ip_ntw(N, PL); t += kIpThreads) {
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(kIpThreads, ip_minblocks(N, PL))
         gstep = (long)gl.ns8 * 2 * 8 * gl.sgc;  // doubles between consecutive m
         swz = gt_swz(gl.ntc, j & 7);
         gcol = 10 * bl;
-        last_state = bl == min(gl.spg, (int)gridDim.y - z * gl.spg) - 1;
+        last_state = bl == min(gl.spg, (int)gridDim.x - z * gl.spg) - 1;
     }
     for (int k = threadIdx.x; k <= R; k += kIpThreads) {
         const double2 w = __ldg(post + k);
@@ -396,7 +399,8 @@ bool eval_ip(const pswe_plan& P, const pswe_params& prm, const double2* fin, dou
                                        (int)cudaSharedmemCarveoutMaxShared));
         attr = true;
     }
-    launch_pdl(kern, dim3(P.nlat, n), dim3(kIpThreads), sm, st, P.R, P.nlat, PL ? P.d_fft_iptw1 : P.d_fft_iptw,
+    launch_pdl(kern, GT ? dim3(n, P.nlat) : dim3(P.nlat, n), dim3(kIpThreads), sm, st, P.R, P.nlat,
+               PL ? P.d_fft_iptw1 : P.d_fft_iptw,
                P.d_fft_post, fin, fout,
                P.d_rowc, P.d_roww, P.d_rowmu, prm.phi_bar, prm.omega, 1.0 / prm.radius, gl);
     PSWE_LAUNCH_CHECK();
