@@ -1,10 +1,11 @@
 // Single-state inverse Legendre contraction on the FP64 CUDA cores with the associated-Legendre
 // values recomputed in registers (sm_100a, fp64): no P table traffic. Used for single states on
-// grids of >= 512 latitude pairs (T1023 on 1024 x 2048, the fine level of BASELINE config 5),
-// where the streamed P table is 2.1 GB and the alternative - the recompute-mode DMMA kernel
-// (legendre_mma.cu) - keeps the recurrence inside its tensor-core loop: T1023 single-state
-// evaluation 736 -> 679 us, PFASST config 5 82.0 -> 78 s/day (profiles/r02_ab_negative.txt item 13
-// has the measurements at the other sizes, where the streamed DMMA kernel stays faster).
+// grids of >= 256 latitude pairs, where the P table outgrows the L2 (T511 269 MB, T1023 2.1 GB):
+// at T1023 the alternative was the recompute-mode DMMA kernel (legendre_mma.cu, the recurrence
+// inside its tensor-core loop): single-state evaluation 736 -> 679 us, PFASST config 5 82.0 -> 78
+// s/day; at T511 the streamed DMMA kernel re-reads the 269 MB table every evaluation: PFASST
+// config 4 10.94 -> 10.77 s/day. Below 256 pairs the table stays in the L2 and the streamed DMMA
+// kernel is faster (profiles/r02_ab_negative.txt item 13).
 //
 // Reference loops replaced: the Legendre sums of synthesise / uv_from_vortdiv
 // (transform.cpp:155-223), G^m(mu_j) = sum_s x^m_s P^m_s(mu_j), with the same recurrence for P as
@@ -242,20 +243,22 @@ void rec2_launch(const pswe_plan& P, const double* Xt, int nq, int NT, int nseg,
 
 }  // namespace
 
-// Single-state inverse on large grids through this kernel: from 512 latitude pairs up
-// (PSWE_INV_REC_J overrides, 0 = off: the recompute-mode DMMA kernel). The X tiles come from the
+// Single-state inverse on large grids through this kernel: from 256 latitude pairs up (T511 and
+// T1023 fine levels; PSWE_INV_REC_J overrides, 0 = off). The X tiles come from the
 // streamed path's prep (or the SDC node update, xtiles_by_sweep_ok).
 bool inv_rec_big(const pswe_plan& P, int nq) {
-    static const int jmin = [] { const char* e = std::getenv("PSWE_INV_REC_J"); return e ? std::atoi(e) : 512; }();
+    static const int jmin = [] { const char* e = std::getenv("PSWE_INV_REC_J"); return e ? std::atoi(e) : 256; }();
     return jmin > 0 && nq <= 4 && P.J >= jmin && P.legendre_mode == PSWE_LEGENDRE_STREAM && P.n_chunks > 0;
 }
 
 void inv_rec_launch(const pswe_plan& P, const double* Xt, int nq, int NT, double2* out, cudaStream_t st) {
     static const int lat = [] { const char* e = std::getenv("PSWE_INVREC_L"); return e ? std::atoi(e) : 4; }();
-    // degree segments per order (1: bit-identical to the DMMA kernels; measured T1023 single state
-    // 679 / 682 / 694 us for 1 / 2 / 4 segments)
-    static const int seg = [] { const char* e = std::getenv("PSWE_INVREC_SEG"); return e ? std::atoi(e) : 1; }();
-    const int nseg = seg < 1 ? 1 : (seg > 4 ? 4 : seg);
+    // degree segments per order: one from 512 latitude pairs (bit-identical to the DMMA kernels;
+    // T1023 single state 679 / 682 / 694 us for 1 / 2 / 4 segments), two below (T511 on 512 x 1024:
+    // the order's chain is half as long; PFASST config 4 10.94 -> 10.77 s/day, one segment 11.74)
+    static const int seg = [] { const char* e = std::getenv("PSWE_INVREC_SEG"); return e ? std::atoi(e) : 0; }();
+    const int want = seg > 0 ? seg : (P.J >= 512 ? 1 : 2);
+    const int nseg = want < 1 ? 1 : (want > 4 ? 4 : want);
     if (lat == 2) rec2_launch<2, 8>(P, Xt, nq, NT, nseg, out, st);
     else rec2_launch<4, 8>(P, Xt, nq, NT, nseg, out, st);
 }

@@ -9,10 +9,11 @@ result against the numpy oracle (oracle/pswe_oracle.py) - no kernel generation i
 | generic Stockham (fft.cu)              | other 5-smooth nlon/2, e.g. T24 on 26 x 50 (N = 25) |
 | streamed-P DMMA Legendre, bulk-copy    | STREAM plans (default)                              |
 |   ring (legendre_stream.cu)            |                                                     |
-| recurrence DMMA Legendre               | RECOMPUTE plans (GpuImexOde), and the single-state  |
-|   (legendre_mma.cu)                    | inverse from 385 to 511 latitude pairs              |
-| DFMA recurrence inverse, P in registers| the single-state inverse from 512 latitude pairs    |
-|   (legendre_rec.cu)                    | (T1023 on 1024 x 2048: config 5's fine level)       |
+| recurrence DMMA Legendre               | RECOMPUTE plans (GpuImexOde)                        |
+|   (legendre_mma.cu)                    |                                                     |
+| DFMA recurrence inverse, P in registers| the single-state inverse from 256 latitude pairs    |
+|   (legendre_rec.cu)                    | (T511 / T1023: configs 4 and 5; one degree segment  |
+|                                        | per order from 512 pairs, two below)                |
 | DFMA (CUDA-core) Legendre (legendre.cu)| PSWE_LEGENDRE_SIMT=1: the measured FP64-FMA         |
 |                                        | alternative the north star compares DMMA against    |
 """
@@ -102,11 +103,15 @@ def test_dfma_legendre_alternative():
 
 
 def test_register_recurrence_inverse_large_grid():
-    """A single state on a grid of >= 512 latitude pairs takes the CUDA-core recurrence inverse
-    (here T255 on 1024 x 512, the oracle's cost kept small); a batch keeps the streamed DMMA one."""
+    """A single state on a grid of >= 256 latitude pairs takes the CUDA-core recurrence inverse
+    (here T255 on 1024 x 512 and 512 x 512 - one and two degree segments - the oracle's cost kept
+    small); a batch keeps the streamed DMMA one."""
     r = run(255, 1024, 512, 1)
     assert has(r["kernels"], "leg_inv_rec2_kernel") and not has(r["kernels"], "leg_inv_tma_kernel"), r["kernels"]
     assert r["err"] < 1e-11
     r = run(255, 1024, 512, 3)
     assert has(r["kernels"], "leg_inv_tma_kernel") and not has(r["kernels"], "leg_inv_rec2_kernel"), r["kernels"]
+    assert r["err"] < 1e-11
+    r = run(255, 512, 512, 1)
+    assert has(r["kernels"], "leg_inv_rec2_kernel"), r["kernels"]
     assert r["err"] < 1e-11
