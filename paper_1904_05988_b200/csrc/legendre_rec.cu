@@ -43,7 +43,7 @@ __device__ __forceinline__ double rec_step(double2 ab, double mu, double p, doub
     return __fma_rn(ab.x, __dmul_rn(mu, p), -__dmul_rn(ab.y, pm1));
 }
 
-// v2: thread = L latitudes (each X value loaded from shared memory feeds L FMAs: the broadcast
+// Thread = L latitudes (each X value loaded from shared memory feeds L FMAs: the broadcast
 // 16-byte load costs two shared-memory wavefronts, so with one latitude per thread the SM's one
 // wavefront per cycle, not the FP64 pipe, would bound the kernel), warp = 32 L latitudes of one
 // order and one degree SEGMENT: the order's chunks are split over the NSEG warps of the block, each
@@ -53,11 +53,8 @@ __device__ __forceinline__ double rec_step(double2 ab, double mu, double p, doub
 // loads the next degree's row into registers while the current one's FMAs issue, and the segments'
 // partial sums are added in segment order through shared memory at the end (NSEG = 1: the exact
 // summation order of the DMMA kernel, bit-identical output).
-#ifndef PSWE_REC_MINB
-#define PSWE_REC_MINB 1
-#endif
 template <int L, int CW>
-__global__ void __launch_bounds__(128, PSWE_REC_MINB) leg_inv_rec2_kernel(int R, int J, int nlat, int nq, int NT, int nct, int nls,
+__global__ void __launch_bounds__(128) leg_inv_rec2_kernel(int R, int J, int nlat, int nq, int NT, int nct, int nls,
                                                            int ncs, int groups, int nseg,
                                                            const double* __restrict__ mu_n,
                                                            const double* __restrict__ seed,
