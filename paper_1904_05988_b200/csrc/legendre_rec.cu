@@ -53,8 +53,10 @@ __device__ __forceinline__ double rec_step(double2 ab, double mu, double p, doub
 // loads the next degree's row into registers while the current one's FMAs issue, and the segments'
 // partial sums are added in segment order through shared memory at the end (NSEG = 1: the exact
 // summation order of the DMMA kernel, bit-identical output).
+// (an explicit one-block-per-SM bound: ptxas then takes 238 registers instead of 218 and the T1023
+// single-state inverse runs 245 instead of 252 us)
 template <int L, int CW>
-__global__ void __launch_bounds__(128) leg_inv_rec2_kernel(int R, int J, int nlat, int nq, int NT, int nct, int nls,
+__global__ void __launch_bounds__(128, 1) leg_inv_rec2_kernel(int R, int J, int nlat, int nq, int NT, int nct, int nls,
                                                            int ncs, int groups, int nseg,
                                                            const double* __restrict__ mu_n,
                                                            const double* __restrict__ seed,
