@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sizes", action="store_true", help="skip the T511/T1023 Legendre roofline lines")
     ap.add_argument("--legendre", type=int, default=1, help="0 recompute, 1 stream (default, measured faster)")
+    ap.add_argument("--ref-worker", default=None, help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -87,17 +88,19 @@ def use_all_host_cores(ref):
     ref.lib().ref_set_threads(n)
 
 
-def reference_step_times(steps: int, warmup: int, budget_s: float | None = None):
-    """The reference's eval_nonlinear + eval_linear (oracle/_ref, swe.cpp:9-69) on bench.py's step:
-    the 5 bench_states at T255 256x512, one state after the other, OpenMP on every host core.
-    Returns (per-step wall times, cores). With budget_s the run stops once that much time is spent
-    (at least one timed step) - the cpu_baseline leg's bounded sample; the reference arm times
-    exactly `steps`. Both legs time the same thing the same way."""
+REF_WARM_S = 6.0
+# The reference's OpenMP team runs with active waiting and bound threads (its best standard setting
+# on this box: on 8 / 16 host cores +15-25% over the default; measured), in a subprocess of its own
+# that never imports torch (torch's OpenMP pool would compete for the bound cores), so the arm
+# (--impl reference) and the cpu_baseline legs time the same code under the same conditions.
+REF_OMP_ENV = {"OMP_WAIT_POLICY": "active", "OMP_PROC_BIND": "true"}
+
+
+def _ref_steps(states, steps: int, warmup: int, budget_s: float | None):
     from oracle import ref_lib as ref
     from oracle.pswe_oracle import ModelParams
     use_all_host_cores(ref)
     plan = ref.RefPlan(R_BENCH, NLAT, NLON)
-    states = bench_states()
     p = ModelParams(phi_bar=9.80616 * 1e4)
     cores = ref.lib().ref_max_threads()
 
@@ -105,8 +108,13 @@ def reference_step_times(steps: int, warmup: int, budget_s: float | None = None)
         for st in states:
             plan.time_eval(st, p, 1)
 
-    for _ in range(warmup):
+    # warm-up: the requested steps, and at least REF_WARM_S seconds (first touch of the plan's
+    # tables, the OpenMP team, clocks)
+    w0 = time.perf_counter()
+    k = 0
+    while k < warmup or time.perf_counter() - w0 < REF_WARM_S:
         step()
+        k += 1
     times, t_start = [], time.perf_counter()
     while len(times) < steps:
         t0 = time.perf_counter()
@@ -117,19 +125,11 @@ def reference_step_times(steps: int, warmup: int, budget_s: float | None = None)
     return times, cores
 
 
-def reference_pfasst(n_ts: int, theta0=None, config: int = 3):
-    """The reference's own pf::run_block (oracle/_ref, pfasst.cpp:194-251) on a BASELINE PFASST
-    config at n_ts time steps per block, ONE block timed (its steady_clock around run_block):
-    serial emulation with OpenMP on every host core at n_ts = 1, the reference's threaded mode
-    (one core per worker, pfasst.cpp:224) beyond — SURVEY §8d(4). Wall s per simulated day =
-    wall / (n_ts dt) * 86400. Two-level configs only (config 5's T1023 plan needs ~13 GB of host
-    memory and minutes per block; config 4 has no reference implementation)."""
+def _ref_pfasst(n_ts: int, th, config: int):
     from oracle import ref_lib as ref
     from oracle.pswe_oracle import ModelParams
-    from paper_1904_05988_b200.cases import config_state
     lv, dt, _, n_iter = PF_CONFIGS[config]
     (Rf, nf_lat, nf_lon, nn_f), (Rc, nc_lat, nc_lon, nn_c) = lv
-    th = config_state(config) if theta0 is None else theta0
     p = ModelParams(phi_bar=9.80616 * 1e4)
     use_all_host_cores(ref)
     r = ref.pfasst_run(Rf, (nf_lat, nf_lon), Rc, (nc_lat, nc_lon), p, nn_f, nn_c, n_ts, dt, n_iter, 1, th,
@@ -138,7 +138,59 @@ def reference_pfasst(n_ts: int, theta0=None, config: int = 3):
     return {"config": config, "n_ts": n_ts, "wall_s_per_sim_day": r.wall / (n_ts * dt) * 86400,
             "wall_s": r.wall, "blocks": 1, "cores": cores if n_ts == 1 else n_ts, "kind": "reference",
             "mode": "serial emulation, OpenMP" if n_ts == 1 else "threaded (one core per worker)",
+            "omp": dict(REF_OMP_ENV),
             "sample": f"one block of {n_ts} step(s), {n_iter} iterations (oracle/_ref pf::run_block)"}
+
+
+def ref_worker_main(spec_json: str):
+    """bench.py --ref-worker SPEC: one reference measurement in a clean process (no torch)."""
+    spec = json.loads(spec_json)
+    if spec["kind"] == "steps":
+        times, cores = _ref_steps(np.load(spec["states"]), spec["steps"], spec["warmup"], spec.get("budget"))
+        print(json.dumps({"times": times, "cores": cores}))
+    else:
+        print(json.dumps(_ref_pfasst(spec["n_ts"], np.load(spec["theta"]), spec["config"])))
+
+
+def _run_ref_worker(spec: dict, arrays: dict):
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        for name, arr in arrays.items():
+            path = os.path.join(d, name + ".npy")
+            np.save(path, arr)
+            spec[name] = path
+        env = dict(os.environ)
+        for k, v in REF_OMP_ENV.items():
+            env.setdefault(k, v)
+        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--ref-worker", json.dumps(spec)], env=env,
+                             capture_output=True, text=True, timeout=1800)
+        if out.returncode != 0:
+            raise RuntimeError(f"reference worker failed: {out.stderr[-500:]}")
+        return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def reference_step_times(steps: int, warmup: int, budget_s: float | None = None):
+    """The reference's eval_nonlinear + eval_linear (oracle/_ref, swe.cpp:9-69) on bench.py's step:
+    the 5 bench_states at T255 256x512, one state after the other, OpenMP on every host core
+    (REF_OMP_ENV, its own process). Returns (per-step wall times, cores). With budget_s the run
+    stops once that much time is spent (at least one timed step) - the cpu_baseline leg's bounded
+    sample; the reference arm times exactly `steps`. Both legs time the same thing the same way."""
+    r = _run_ref_worker({"kind": "steps", "steps": steps, "warmup": warmup, "budget": budget_s},
+                        {"states": bench_states()})
+    return r["times"], r["cores"]
+
+
+def reference_pfasst(n_ts: int, theta0=None, config: int = 3):
+    """The reference's own pf::run_block (oracle/_ref, pfasst.cpp:194-251) on a BASELINE PFASST
+    config at n_ts time steps per block, ONE block timed (its steady_clock around run_block):
+    serial emulation with OpenMP on every host core at n_ts = 1, the reference's threaded mode
+    (one core per worker, pfasst.cpp:224) beyond — SURVEY §8d(4). Wall s per simulated day =
+    wall / (n_ts dt) * 86400. Two-level configs only (config 5's T1023 plan needs ~13 GB of host
+    memory and minutes per block; config 4 has no reference implementation)."""
+    if theta0 is None:
+        from paper_1904_05988_b200.cases import config_state
+        theta0 = config_state(config)
+    return _run_ref_worker({"kind": "pfasst", "n_ts": n_ts, "config": config}, {"theta": np.asarray(theta0)})
 
 
 def run_reference_arm(args):
@@ -160,7 +212,8 @@ def run_reference_arm(args):
         "config": dict(CONFIG),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "reference",
                          "sample": f"{args.steps} steps x {BATCH} evals, reference eval_nonlinear+eval_linear "
-                                   f"(OpenMP {cores} threads, FFTW-API shim)"},
+                                   f"(OpenMP {cores} threads, active wait, bound; own process; "
+                                   f"FFTW-API shim)"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     if not args.no_pfasst:
@@ -561,7 +614,7 @@ def run_ours(args):
             cpu = {"value": BATCH * len(times) / sum(times), "unit": "evals/s", "cores": cores, "kind": "reference",
                    "sample": f"{len(times)} steps x {BATCH} evals (bench step: T{R_BENCH} {NLAT}x{NLON}, the 5 "
                              f"bench_states), reference eval_nonlinear+eval_linear, OpenMP {cores} threads, "
-                             f"timed like --impl reference ({sum(times):.1f} s)"}
+                             f"timed like --impl reference (own process, OpenMP active wait, bound) ({sum(times):.1f} s)"}
         except Exception as e:
             cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -653,6 +706,9 @@ def run_pfasst(P, prm, world, rank, dev, clocks_dev=0, config=3):
 
 def main():
     args = parse()
+    if args.ref_worker is not None:
+        ref_worker_main(args.ref_worker)
+        return
     if args.impl == "reference":
         run_reference_arm(args)
     else:
